@@ -1,0 +1,156 @@
+/*
+ * irdn.h — C ABI of the B200-native FNR (Fast Noise Reduction) filter.
+ *
+ * This is the drop-in boundary for the reference's filter entry points
+ * (irdenoise v0.1.0, pure Python). Every function here replaces one
+ * reference interface; the citation is given beside each declaration
+ * (paths relative to the reference checkout, pkg/src/irdenoise/...):
+ *
+ *   irdn_run_filter_u8 / _u16     <- filters.py:79-102   run_filter(img, spec, method, passes, threads)
+ *   irdn_filter_pass_u8 / _u16    <- filters.py:69-76    fnr_pass / mf_pass  (one pass, caller's stats)
+ *                                    filters.py:105-127  _run_rows_threaded  (fresh out buffer, counter merge)
+ *                                    filters.py:130-181  _filter_rows        (gather, detect, median, write)
+ *   irdn_filter_strip_u8 / _u16   <- filters.py:130      _filter_rows(img, k, y0, y1, ...) row range [y0, y1)
+ *                                    of a frame whose rows are clamped against the GLOBAL image height
+ *   irdn_stats                    <- filters.py:33-52    FilterStats (same field meaning and key order)
+ *   IRDN_METHOD_FNR / _MF         <- filters.py:23-24    METHOD_FNR = "fnr", METHOD_MF = "mf"
+ *
+ * Semantics (bit-exact with the reference):
+ *   - row-major frames, origin top-left; replicate-edge (clamp) window gather;
+ *   - FNR: a pixel is noisy iff it equals the min or the max of its k x k
+ *     window (centre included); noisy pixels become the window median
+ *     (element (k*k-1)/2 of the sorted window), signal pixels are copied;
+ *   - MF: every pixel becomes the window median;
+ *   - a pass reads an immutable input and writes a distinct output buffer.
+ *
+ * Counters: the device pass entry points ADD to d_counts[0] (= detected,
+ * which also equals FNR sorts) and d_counts[1] (= replacements). For MF both
+ * stay untouched (sorts = pixels x passes, as the reference counts them).
+ *
+ * Error handling: every entry point returns IRDN_OK (0) or an error code;
+ * irdn_last_error() returns the thread-local message of the last failure.
+ * Argument errors (IRDN_EINVAL) mirror the reference's ValueErrors
+ * (filters.py:90-93 bad method / passes; image.py:63-65 bad k;
+ * image.py:30-36 bad image dimensions). There is no CPU fallback: without a
+ * usable sm_100 device every compute call fails with IRDN_ENODEV.
+ *
+ * Streams are passed as void* (a cudaStream_t / CUstream; NULL = legacy
+ * default stream). Device pointers must be device-resident (cudaMalloc /
+ * torch); host pointers in irdn_run_filter_* may be pageable or pinned.
+ */
+#ifndef IRDN_H_
+#define IRDN_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define IRDN_API __attribute__((visibility("default")))
+#else
+#define IRDN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IRDN_OK 0
+#define IRDN_EINVAL 1   /* invalid argument: the reference raises ValueError */
+#define IRDN_ECUDA 2    /* CUDA runtime / launch failure */
+#define IRDN_ENODEV 3   /* no usable sm_100 device */
+
+#define IRDN_METHOD_FNR 0  /* filters.py:23  METHOD_FNR = "fnr" */
+#define IRDN_METHOD_MF 1   /* filters.py:24  METHOD_MF = "mf"   */
+
+/* Mirrors FilterStats (filters.py:33-52). elapsed_ms is wall time of the call. */
+typedef struct irdn_stats {
+  uint64_t minmax_scans;
+  uint64_t sorts;
+  uint64_t replacements;
+  uint64_t detected;
+  double elapsed_ms;
+  uint64_t passes;
+} irdn_stats;
+
+/* Library identity / capability queries. */
+IRDN_API const char* irdn_version(void);
+IRDN_API const char* irdn_last_error(void);
+/* Number of visible CUDA devices of compute capability 10.x (0 when none). */
+IRDN_API int irdn_device_count(void);
+/* Bit mask of window sides with a specialised kernel (bit k set => k fast path). */
+IRDN_API uint64_t irdn_fast_window_mask(int32_t bytes_per_pixel);
+
+/*
+ * One filter pass over `batch` frames of height x width, device-resident,
+ * stream-ordered and asynchronous (no host sync).
+ *   in_pitch / out_pitch: row pitch in ELEMENTS; frames are contiguous blocks
+ *   of height*pitch elements. d_in and d_out must not overlap.
+ * Replaces fnr_pass / mf_pass (filters.py:69-76) for one frame per batch entry.
+ */
+IRDN_API int irdn_filter_pass_u8(const uint8_t* d_in, uint8_t* d_out, int64_t batch, int64_t height,
+                        int64_t width, int64_t in_pitch, int64_t out_pitch, int32_t k,
+                        int32_t method, unsigned long long* d_counts, void* stream);
+IRDN_API int irdn_filter_pass_u16(const uint16_t* d_in, uint16_t* d_out, int64_t batch, int64_t height,
+                         int64_t width, int64_t in_pitch, int64_t out_pitch, int32_t k,
+                         int32_t method, unsigned long long* d_counts, void* stream);
+
+/*
+ * Row-strip pass for one frame of GLOBAL size height x width (multi-GPU row
+ * strips, BASELINE config 4): computes output rows [row_begin, row_end).
+ *   d_in   points at global row in_row0 and holds in_rows rows; it must cover
+ *          [max(0,row_begin-k/2), min(height,row_end+k/2)) — window rows are
+ *          clamped against the global image, exactly like _filter_rows(y0, y1)
+ *          (filters.py:130-157), never against the strip.
+ *   d_out  points at the output row row_begin (row_end-row_begin rows).
+ */
+IRDN_API int irdn_filter_strip_u8(const uint8_t* d_in, int64_t in_row0, int64_t in_rows, uint8_t* d_out,
+                         int64_t row_begin, int64_t row_end, int64_t height, int64_t width,
+                         int64_t in_pitch, int64_t out_pitch, int32_t k, int32_t method,
+                         unsigned long long* d_counts, void* stream);
+IRDN_API int irdn_filter_strip_u16(const uint16_t* d_in, int64_t in_row0, int64_t in_rows,
+                          uint16_t* d_out, int64_t row_begin, int64_t row_end, int64_t height,
+                          int64_t width, int64_t in_pitch, int64_t out_pitch, int32_t k,
+                          int32_t method, unsigned long long* d_counts, void* stream);
+
+/*
+ * Whole run_filter (filters.py:79-102) over HOST buffers: validation, H2D,
+ * `passes` passes on `device` (each pass reading the previous output), D2H,
+ * and the FilterStats counters. Copies are pipelined against the filter in
+ * frame chunks (or row strips for a single frame) on internal streams.
+ * h_in and h_out must not overlap; batch frames are contiguous (pitch=width).
+ */
+IRDN_API int irdn_run_filter_u8(const uint8_t* h_in, uint8_t* h_out, int64_t batch, int64_t height,
+                       int64_t width, int32_t k, int32_t method, int32_t passes,
+                       int32_t device, irdn_stats* stats);
+IRDN_API int irdn_run_filter_u16(const uint16_t* h_in, uint16_t* h_out, int64_t batch, int64_t height,
+                        int64_t width, int32_t k, int32_t method, int32_t passes,
+                        int32_t device, irdn_stats* stats);
+
+/*
+ * run_filter over DEVICE buffers, stream-ordered: `passes` passes from d_in
+ * to d_out, ping-ponging through d_tmp (required when passes > 1, same size
+ * as d_out). Counters are added to d_counts[0..1] (see above).
+ */
+IRDN_API int irdn_run_filter_device_u8(const uint8_t* d_in, uint8_t* d_out, uint8_t* d_tmp,
+                              int64_t batch, int64_t height, int64_t width, int32_t k,
+                              int32_t method, int32_t passes, unsigned long long* d_counts,
+                              void* stream);
+IRDN_API int irdn_run_filter_device_u16(const uint16_t* d_in, uint16_t* d_out, uint16_t* d_tmp,
+                               int64_t batch, int64_t height, int64_t width, int32_t k,
+                               int32_t method, int32_t passes, unsigned long long* d_counts,
+                               void* stream);
+
+/* Kernel launches issued by this thread since the last reset (for bench accounting). */
+IRDN_API uint64_t irdn_launch_count(void);
+IRDN_API void irdn_reset_launch_count(void);
+
+/*
+ * Force the generic (non-specialised) kernel for testing: 1 = generic only,
+ * 0 = normal dispatch. Returns the previous value. Process-wide.
+ */
+IRDN_API int32_t irdn_set_force_generic(int32_t on);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IRDN_H_ */

@@ -1,0 +1,431 @@
+// C-ABI of the B200 FNR filter (declared in include/irdn.h).
+//
+// Host-side mirror of the reference driver (pkg/src/irdenoise/filters.py):
+//   run_filter        filters.py:79-102   -> irdn_run_filter_{u8,u16} (host buffers)
+//                                            irdn_run_filter_device_{u8,u16} (device buffers)
+//   fnr_pass/mf_pass  filters.py:69-76    -> irdn_filter_pass_{u8,u16}
+//   _filter_rows(y0,y1) filters.py:130    -> irdn_filter_strip_{u8,u16}
+// There is no CPU fallback anywhere in this file: every compute entry point
+// launches sm_100a kernels or fails with IRDN_ENODEV / IRDN_ECUDA.
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/irdn.h"
+#include "fnr_common.cuh"
+#include "fnr_generic.cuh"
+#include "fnr_fast.cuh"
+
+namespace irdn {
+
+static thread_local std::string g_err;
+static thread_local uint64_t g_launches = 0;
+static int32_t g_force_generic = 0;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define IRDN_CUDA(call)                                                                      \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(IRDN_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),        \
+                  __FILE__, __LINE__);                                                       \
+  } while (0)
+
+void note_launch() { ++g_launches; }
+
+// Cached per-device check: only compute capability 10.x runs the sm_100a code.
+static int check_device(int* dev_out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(IRDN_ENODEV, "no CUDA device: %s", cudaGetErrorString(e));
+  static int cc_major[64] = {0};
+  if (dev < 64 && cc_major[dev] == 0) {
+    int major = -1;
+    e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e != cudaSuccess) return fail(IRDN_ENODEV, "device query failed: %s", cudaGetErrorString(e));
+    cc_major[dev] = major;
+  }
+  if (dev >= 64 || cc_major[dev] != 10)
+    return fail(IRDN_ENODEV, "device %d is not an sm_100 (B200) device", dev);
+  if (dev_out) *dev_out = dev;
+  return IRDN_OK;
+}
+
+// Validation mirroring the reference's ValueErrors.
+static int validate(int64_t batch, int64_t height, int64_t width, int32_t k, int32_t method) {
+  if (method != IRDN_METHOD_FNR && method != IRDN_METHOD_MF)  // filters.py:90-91
+    return fail(IRDN_EINVAL, "unknown method %d, expected 'fnr' or 'mf'", method);
+  if (k < 3 || k % 2 == 0)  // image.py:63-65
+    return fail(IRDN_EINVAL, "window side must be an odd integer >= 3, got %d", k);
+  if (width < 1 || height < 1)  // image.py:30-31
+    return fail(IRDN_EINVAL, "image dimensions must be >= 1, got %lldx%lld", (long long)width,
+                (long long)height);
+  if (batch < 1) return fail(IRDN_EINVAL, "batch must be >= 1, got %lld", (long long)batch);
+  if (height > INT32_MAX / 2 || width > INT32_MAX / 2 || k > 4095)
+    return fail(IRDN_EINVAL, "frame %lldx%lld or window %d too large", (long long)width,
+                (long long)height, k);
+  return IRDN_OK;
+}
+
+static bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  const char* pa = (const char*)a;
+  const char* pb = (const char*)b;
+  return pa < pb + nb && pb < pa + na;
+}
+
+template <typename T>
+static int launch_pass(const T* d_in, T* d_out, const PassGeom& g, int k, int method,
+                       unsigned long long* d_counts, cudaStream_t s) {
+  if (!g_force_generic) {
+    int rc = -1;
+    if (fast::try_launch<T>(d_in, d_out, g, k, method, d_counts, s, &rc)) {
+      if (rc != IRDN_OK) return fail(IRDN_ECUDA, "fast kernel launch failed: %s", fast::last_error());
+      note_launch();
+      return IRDN_OK;
+    }
+  }
+  const int rows = g.row_end - g.row_begin;
+  dim3 grid((g.width + 31) / 32, (rows + 7) / 8, std::min<int>(g.batch, 65535));
+  if (grid.y > 65535u) return fail(IRDN_EINVAL, "frame too tall for the generic kernel");
+  fnr_generic_kernel<T><<<grid, 256, 0, s>>>(d_in, d_out, g, k, method, d_counts);
+  IRDN_CUDA(cudaGetLastError());
+  note_launch();
+  return IRDN_OK;
+}
+
+template <typename T>
+static int filter_pass(const T* d_in, T* d_out, int64_t batch, int64_t height, int64_t width,
+                       int64_t in_pitch, int64_t out_pitch, int32_t k, int32_t method,
+                       unsigned long long* d_counts, void* stream) {
+  int rc = validate(batch, height, width, k, method);
+  if (rc) return rc;
+  if (!d_in || !d_out) return fail(IRDN_EINVAL, "null buffer");
+  if (in_pitch < width || out_pitch < width) return fail(IRDN_EINVAL, "pitch smaller than width");
+  if (method == IRDN_METHOD_FNR && !d_counts) return fail(IRDN_EINVAL, "FNR needs d_counts[2]");
+  const size_t in_bytes = (size_t)((batch - 1) * height * in_pitch + (height - 1) * in_pitch + width) * sizeof(T);
+  const size_t out_bytes = (size_t)((batch - 1) * height * out_pitch + (height - 1) * out_pitch + width) * sizeof(T);
+  if (overlaps(d_in, in_bytes, d_out, out_bytes))
+    return fail(IRDN_EINVAL, "input and output buffers overlap (a pass never sees its own writes)");
+  if ((rc = check_device(nullptr))) return rc;
+  PassGeom g;
+  g.in_frame_stride = height * in_pitch;
+  g.out_frame_stride = height * out_pitch;
+  g.in_pitch = in_pitch;
+  g.out_pitch = out_pitch;
+  g.height = (int32_t)height;
+  g.width = (int32_t)width;
+  g.in_row0 = 0;
+  g.in_rows = (int32_t)height;
+  g.row_begin = 0;
+  g.row_end = (int32_t)height;
+  g.batch = (int32_t)batch;
+  return launch_pass<T>(d_in, d_out, g, k, method, d_counts, (cudaStream_t)stream);
+}
+
+template <typename T>
+static int filter_strip(const T* d_in, int64_t in_row0, int64_t in_rows, T* d_out,
+                        int64_t row_begin, int64_t row_end, int64_t height, int64_t width,
+                        int64_t in_pitch, int64_t out_pitch, int32_t k, int32_t method,
+                        unsigned long long* d_counts, void* stream) {
+  int rc = validate(1, height, width, k, method);
+  if (rc) return rc;
+  if (!d_in || !d_out) return fail(IRDN_EINVAL, "null buffer");
+  if (in_pitch < width || out_pitch < width) return fail(IRDN_EINVAL, "pitch smaller than width");
+  if (method == IRDN_METHOD_FNR && !d_counts) return fail(IRDN_EINVAL, "FNR needs d_counts[2]");
+  if (row_begin < 0 || row_end > height || row_begin >= row_end)
+    return fail(IRDN_EINVAL, "bad output row range [%lld, %lld) for height %lld",
+                (long long)row_begin, (long long)row_end, (long long)height);
+  const int64_t r = k / 2;
+  const int64_t need0 = std::max<int64_t>(0, row_begin - r);
+  const int64_t need1 = std::min<int64_t>(height, row_end + r);
+  if (in_row0 > need0 || in_row0 + in_rows < need1 || in_row0 < 0 || in_row0 + in_rows > height)
+    return fail(IRDN_EINVAL,
+                "input strip rows [%lld, %lld) do not cover the clamped window rows [%lld, %lld)",
+                (long long)in_row0, (long long)(in_row0 + in_rows), (long long)need0, (long long)need1);
+  if ((rc = check_device(nullptr))) return rc;
+  PassGeom g;
+  g.in_frame_stride = in_rows * in_pitch;
+  g.out_frame_stride = (row_end - row_begin) * out_pitch;
+  g.in_pitch = in_pitch;
+  g.out_pitch = out_pitch;
+  g.height = (int32_t)height;
+  g.width = (int32_t)width;
+  g.in_row0 = (int32_t)in_row0;
+  g.in_rows = (int32_t)in_rows;
+  g.row_begin = (int32_t)row_begin;
+  g.row_end = (int32_t)row_end;
+  g.batch = 1;
+  return launch_pass<T>(d_in, d_out, g, k, method, d_counts, (cudaStream_t)stream);
+}
+
+// passes > 1: pass i reads pass i-1's output (filters.py:96-100). Buffers are
+// chosen so the LAST pass lands in d_out.
+template <typename T>
+static int run_device(const T* d_in, T* d_out, T* d_tmp, int64_t batch, int64_t height,
+                      int64_t width, int32_t k, int32_t method, int32_t passes,
+                      unsigned long long* d_counts, void* stream) {
+  if (passes < 1) return fail(IRDN_EINVAL, "passes must be >= 1, got %d", passes);  // filters.py:92-93
+  if (passes > 1 && !d_tmp) return fail(IRDN_EINVAL, "passes > 1 needs a d_tmp buffer");
+  const T* src = d_in;
+  for (int p = 0; p < passes; ++p) {
+    T* dst = ((passes - 1 - p) % 2 == 0) ? d_out : d_tmp;
+    int rc = filter_pass<T>(src, dst, batch, height, width, width, width, k, method, d_counts, stream);
+    if (rc) return rc;
+    src = dst;
+  }
+  return IRDN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer run_filter with copy/compute pipelining.
+// ---------------------------------------------------------------------------
+struct DeviceWorkspace {
+  std::mutex mu;
+  void* buf = nullptr;  // [in | out | tmp] regions
+  size_t cap = 0;
+  unsigned long long* counts = nullptr;
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  bool ready = false;
+};
+static DeviceWorkspace g_ws[64];
+
+static int ensure_workspace(DeviceWorkspace& ws, size_t bytes) {
+  if (!ws.ready) {
+    IRDN_CUDA(cudaStreamCreateWithFlags(&ws.s_h2d, cudaStreamNonBlocking));
+    IRDN_CUDA(cudaStreamCreateWithFlags(&ws.s_comp, cudaStreamNonBlocking));
+    IRDN_CUDA(cudaStreamCreateWithFlags(&ws.s_d2h, cudaStreamNonBlocking));
+    IRDN_CUDA(cudaMalloc(&ws.counts, 2 * sizeof(unsigned long long)));
+    ws.ready = true;
+  }
+  if (ws.cap < bytes) {
+    if (ws.buf) IRDN_CUDA(cudaFree(ws.buf));
+    ws.buf = nullptr;
+    ws.cap = 0;
+    IRDN_CUDA(cudaMalloc(&ws.buf, bytes));
+    ws.cap = bytes;
+  }
+  return IRDN_OK;
+}
+
+template <typename T>
+static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int64_t width,
+                    int32_t k, int32_t method, int32_t passes, int32_t device, irdn_stats* stats) {
+  auto t0 = std::chrono::steady_clock::now();
+  int rc = validate(batch, height, width, k, method);
+  if (rc) return rc;
+  if (passes < 1) return fail(IRDN_EINVAL, "passes must be >= 1, got %d", passes);
+  if (!h_in || !h_out) return fail(IRDN_EINVAL, "null buffer");
+  const int64_t frame = height * width;
+  const size_t nbytes = (size_t)(batch * frame) * sizeof(T);
+  if (overlaps(h_in, nbytes, h_out, nbytes)) return fail(IRDN_EINVAL, "input and output buffers overlap");
+  if (device < 0 || device >= 64) return fail(IRDN_EINVAL, "bad device %d", device);
+  int prev = 0;
+  IRDN_CUDA(cudaGetDevice(&prev));
+  if (prev != device) IRDN_CUDA(cudaSetDevice(device));
+  struct Restore {
+    int d, p;
+    ~Restore() { if (d != p) cudaSetDevice(p); }
+  } restore{device, prev};
+  if ((rc = check_device(nullptr))) return rc;
+
+  DeviceWorkspace& ws = g_ws[device];
+  std::lock_guard<std::mutex> lock(ws.mu);
+  const int nbuf = passes > 1 ? 3 : 2;
+  if ((rc = ensure_workspace(ws, nbytes * nbuf))) return rc;
+  T* d_in = (T*)ws.buf;
+  T* d_out = d_in + batch * frame;
+  T* d_tmp = passes > 1 ? d_out + batch * frame : nullptr;
+  IRDN_CUDA(cudaMemsetAsync(ws.counts, 0, 2 * sizeof(unsigned long long), ws.s_comp));
+
+  // Chunking: frames for a batch; row strips for a single frame with one pass.
+  const int r = k / 2;
+  struct Chunk { int64_t f0, nf, y0, y1; };
+  std::vector<Chunk> chunks;
+  if (batch >= 2) {
+    const int64_t target = std::max<int64_t>(1, (int64_t)((8u << 20) / sizeof(T)) / frame);  // ~8 MB
+    const int64_t nchunks = std::min<int64_t>(std::max<int64_t>(1, batch / target), 64);
+    for (int64_t i = 0; i < nchunks; ++i) {
+      int64_t a = batch * i / nchunks, b = batch * (i + 1) / nchunks;
+      if (b > a) chunks.push_back({a, b - a, 0, height});
+    }
+  } else if (passes == 1 && height >= 4 * (int64_t)(r + 1) && frame * (int64_t)sizeof(T) >= (16 << 20)) {
+    const int64_t nchunks = std::min<int64_t>(16, height / (4 * (r + 1)));
+    for (int64_t i = 0; i < nchunks; ++i) {
+      int64_t a = height * i / nchunks, b = height * (i + 1) / nchunks;
+      chunks.push_back({0, 1, a, b});
+    }
+  } else {
+    chunks.push_back({0, batch, 0, height});
+  }
+
+  std::vector<cudaEvent_t> ev_in(chunks.size()), ev_done(chunks.size());
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    IRDN_CUDA(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+    IRDN_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
+  }
+  struct EvFree {
+    std::vector<cudaEvent_t>& a; std::vector<cudaEvent_t>& b;
+    ~EvFree() { for (auto e : a) cudaEventDestroy(e); for (auto e : b) cudaEventDestroy(e); }
+  } evfree{ev_in, ev_done};
+
+  const bool row_mode = batch == 1 && chunks.size() > 1;
+  // H2D: each chunk's own rows (row mode: strips, in order).
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    const Chunk& c = chunks[i];
+    const int64_t off = c.f0 * frame + c.y0 * width;
+    const int64_t cnt = row_mode ? (c.y1 - c.y0) * width : c.nf * frame;
+    IRDN_CUDA(cudaMemcpyAsync(d_in + off, h_in + off, cnt * sizeof(T), cudaMemcpyHostToDevice, ws.s_h2d));
+    IRDN_CUDA(cudaEventRecord(ev_in[i], ws.s_h2d));
+  }
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    const Chunk& c = chunks[i];
+    if (row_mode) {
+      // A strip needs the input rows up to y1 + r, i.e. possibly the next chunk's copy.
+      size_t last = i;
+      while (last + 1 < chunks.size() && chunks[last].y1 < std::min<int64_t>(height, c.y1 + r)) ++last;
+      IRDN_CUDA(cudaStreamWaitEvent(ws.s_comp, ev_in[last], 0));
+      const int64_t in0 = std::max<int64_t>(0, c.y0 - r);
+      const int64_t in1 = std::min<int64_t>(height, c.y1 + r);
+      rc = filter_strip<T>(d_in + in0 * width, in0, in1 - in0, d_out + c.y0 * width, c.y0, c.y1,
+                           height, width, width, width, k, method, ws.counts, ws.s_comp);
+      if (rc) return rc;
+    } else {
+      IRDN_CUDA(cudaStreamWaitEvent(ws.s_comp, ev_in[i], 0));
+      const int64_t off = c.f0 * frame;
+      rc = run_device<T>(d_in + off, d_out + off, d_tmp ? d_tmp + off : nullptr, c.nf, height,
+                         width, k, method, passes, ws.counts, ws.s_comp);
+      if (rc) return rc;
+    }
+    IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
+    IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
+    const int64_t off = c.f0 * frame + c.y0 * width;
+    const int64_t cnt = row_mode ? (c.y1 - c.y0) * width : c.nf * frame;
+    IRDN_CUDA(cudaMemcpyAsync(h_out + off, d_out + off, cnt * sizeof(T), cudaMemcpyDeviceToHost, ws.s_d2h));
+  }
+  unsigned long long counts[2] = {0, 0};
+  IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done.back(), 0));
+  IRDN_CUDA(cudaMemcpyAsync(counts, ws.counts, sizeof(counts), cudaMemcpyDeviceToHost, ws.s_d2h));
+  IRDN_CUDA(cudaStreamSynchronize(ws.s_d2h));
+  IRDN_CUDA(cudaStreamSynchronize(ws.s_comp));
+  IRDN_CUDA(cudaGetLastError());
+
+  if (stats) {
+    const uint64_t pixels = (uint64_t)(batch * frame) * (uint64_t)passes;
+    // FilterStats accounting (filters.py:121-126).
+    stats->passes = (uint64_t)passes;
+    if (method == IRDN_METHOD_FNR) {
+      stats->minmax_scans = pixels;
+      stats->detected = counts[0];
+      stats->sorts = counts[0];
+      stats->replacements = counts[1];
+    } else {
+      stats->minmax_scans = 0;
+      stats->detected = 0;
+      stats->sorts = pixels;
+      stats->replacements = 0;
+    }
+    stats->elapsed_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return IRDN_OK;
+}
+
+}  // namespace irdn
+
+using namespace irdn;
+
+extern "C" {
+
+const char* irdn_version(void) { return "irdn-b200 0.1.0 (sm_100a)"; }
+const char* irdn_last_error(void) { return g_err.c_str(); }
+
+int irdn_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int count = 0;
+  for (int d = 0; d < n; ++d) {
+    int major = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d) == cudaSuccess && major == 10)
+      ++count;
+  }
+  return count;
+}
+
+uint64_t irdn_fast_window_mask(int32_t bytes_per_pixel) { return fast::window_mask(bytes_per_pixel); }
+
+int irdn_filter_pass_u8(const uint8_t* d_in, uint8_t* d_out, int64_t batch, int64_t height,
+                        int64_t width, int64_t in_pitch, int64_t out_pitch, int32_t k,
+                        int32_t method, unsigned long long* d_counts, void* stream) {
+  return filter_pass<uint8_t>(d_in, d_out, batch, height, width, in_pitch, out_pitch, k, method,
+                              d_counts, stream);
+}
+int irdn_filter_pass_u16(const uint16_t* d_in, uint16_t* d_out, int64_t batch, int64_t height,
+                         int64_t width, int64_t in_pitch, int64_t out_pitch, int32_t k,
+                         int32_t method, unsigned long long* d_counts, void* stream) {
+  return filter_pass<uint16_t>(d_in, d_out, batch, height, width, in_pitch, out_pitch, k, method,
+                               d_counts, stream);
+}
+int irdn_filter_strip_u8(const uint8_t* d_in, int64_t in_row0, int64_t in_rows, uint8_t* d_out,
+                         int64_t row_begin, int64_t row_end, int64_t height, int64_t width,
+                         int64_t in_pitch, int64_t out_pitch, int32_t k, int32_t method,
+                         unsigned long long* d_counts, void* stream) {
+  return filter_strip<uint8_t>(d_in, in_row0, in_rows, d_out, row_begin, row_end, height, width,
+                               in_pitch, out_pitch, k, method, d_counts, stream);
+}
+int irdn_filter_strip_u16(const uint16_t* d_in, int64_t in_row0, int64_t in_rows,
+                          uint16_t* d_out, int64_t row_begin, int64_t row_end, int64_t height,
+                          int64_t width, int64_t in_pitch, int64_t out_pitch, int32_t k,
+                          int32_t method, unsigned long long* d_counts, void* stream) {
+  return filter_strip<uint16_t>(d_in, in_row0, in_rows, d_out, row_begin, row_end, height, width,
+                                in_pitch, out_pitch, k, method, d_counts, stream);
+}
+int irdn_run_filter_u8(const uint8_t* h_in, uint8_t* h_out, int64_t batch, int64_t height,
+                       int64_t width, int32_t k, int32_t method, int32_t passes, int32_t device,
+                       irdn_stats* stats) {
+  return run_host<uint8_t>(h_in, h_out, batch, height, width, k, method, passes, device, stats);
+}
+int irdn_run_filter_u16(const uint16_t* h_in, uint16_t* h_out, int64_t batch, int64_t height,
+                        int64_t width, int32_t k, int32_t method, int32_t passes,
+                        int32_t device, irdn_stats* stats) {
+  return run_host<uint16_t>(h_in, h_out, batch, height, width, k, method, passes, device, stats);
+}
+int irdn_run_filter_device_u8(const uint8_t* d_in, uint8_t* d_out, uint8_t* d_tmp,
+                              int64_t batch, int64_t height, int64_t width, int32_t k,
+                              int32_t method, int32_t passes, unsigned long long* d_counts,
+                              void* stream) {
+  return run_device<uint8_t>(d_in, d_out, d_tmp, batch, height, width, k, method, passes,
+                             d_counts, stream);
+}
+int irdn_run_filter_device_u16(const uint16_t* d_in, uint16_t* d_out, uint16_t* d_tmp,
+                               int64_t batch, int64_t height, int64_t width, int32_t k,
+                               int32_t method, int32_t passes, unsigned long long* d_counts,
+                               void* stream) {
+  return run_device<uint16_t>(d_in, d_out, d_tmp, batch, height, width, k, method, passes,
+                              d_counts, stream);
+}
+uint64_t irdn_launch_count(void) { return g_launches; }
+void irdn_reset_launch_count(void) { g_launches = 0; }
+int32_t irdn_set_force_generic(int32_t on) {
+  int32_t prev = g_force_generic;
+  g_force_generic = on ? 1 : 0;
+  return prev;
+}
+
+}  // extern "C"
