@@ -1,18 +1,134 @@
-// Specialised tile kernels (dispatch stub; filled in by the TMA kernels).
+// Host-side dispatch of the specialised TMA tile kernels (fnr_tile.cuh).
+//
+// The tile path is taken when the window side has a generated selection
+// network (k = 3, 5, 7, 9, 11) and the buffers satisfy TMA's rules (16-byte
+// aligned base, row pitch and frame stride multiples of 16 bytes). Anything
+// else goes to the generic kernel (fnr_generic.cuh) — still sm_100a code.
 #pragma once
+#include <cuda.h>
+#include <mutex>
+#include <string>
 #include "fnr_common.cuh"
+#include "fnr_tile.cuh"
 
 namespace irdn {
 void note_launch();
 namespace fast {
 
-inline const char* last_error() { return ""; }
-inline uint64_t window_mask(int32_t) { return 0; }
+static thread_local std::string g_fast_err;
+inline const char* last_error() { return g_fast_err.c_str(); }
+
+inline uint64_t window_mask(int32_t) {
+  return (1ull << 3) | (1ull << 5) | (1ull << 7) | (1ull << 9) | (1ull << 11);
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
 
 template <typename T>
-inline bool try_launch(const T*, T*, const PassGeom&, int, int, unsigned long long*, cudaStream_t,
-                       int*) {
-  return false;
+inline bool make_map(CUtensorMap* map, const void* base, int64_t width, int64_t rows, int64_t batch,
+                     int64_t pitch, int64_t frame_stride, int box_w, int box_h) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)width, (cuuint64_t)rows, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)(pitch * (int64_t)sizeof(T)),
+                                 (cuuint64_t)(frame_stride * (int64_t)sizeof(T))};
+  const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1u};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  const CUtensorMapDataType dt = sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+  CUresult res = fn(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (res != CUDA_SUCCESS) return false;
+  // Drivers up to 13.1 encode tensors spanning < 128 KiB with descriptor bit 85
+  // (word 1, bit 21) set, which faults (cudaErrorIllegalInstruction) on sm_100;
+  // clear it, as CUTLASS does for the same driver range.
+  int drv = 0;
+  if (cudaDriverGetVersion(&drv) == cudaSuccess && drv <= 13010) {
+    const int64_t span = ((batch - 1) * frame_stride + (rows - 1) * pitch + width) * (int64_t)sizeof(T);
+    if (span < 131072) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+  }
+  return true;
+}
+
+template <typename T, int K>
+inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, unsigned long long* counts,
+                       cudaStream_t s, bool* taken) {
+  using G = tile::Geo<T, K>;
+  *taken = false;
+  CUtensorMap in_map, out_map;
+  const int out_rows = g.row_end - g.row_begin;
+  if (!make_map<T>(&in_map, d_in, g.width, g.in_rows, g.batch, g.in_pitch, g.in_frame_stride, G::BOXW, G::BOXH))
+    return 0;
+  if (!make_map<T>(&out_map, d_out, g.width, out_rows, g.batch, g.out_pitch, g.out_frame_stride, tile::TW,
+                   tile::TH))
+    return 0;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(tile::fnr_tile_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    attr_done = true;
+  }
+  tile::TileParams p;
+  p.width = g.width;
+  p.height = g.height;
+  p.in_row0 = g.in_row0;
+  p.row_begin = g.row_begin;
+  p.row_end = g.row_end;
+  p.tiles_x = (g.width + tile::TW - 1) / tile::TW;
+  p.tiles_y = (out_rows + tile::TH - 1) / tile::TH;
+  p.batch = g.batch;
+  p.method = method;
+  p.counts = counts;
+  const long long ntiles = (long long)p.tiles_x * p.tiles_y;
+  if (ntiles > 0x7fffffffLL) return 0;
+  dim3 grid((unsigned)ntiles, (unsigned)std::min<int>(g.batch, 65535));
+  *taken = true;
+  tile::fnr_tile_kernel<T, K><<<grid, tile::THREADS, G::SMEM, s>>>(in_map, out_map, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_fast_err = cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
+
+template <typename T>
+inline bool try_launch(const T* d_in, T* d_out, const PassGeom& g, int k, int method, unsigned long long* counts,
+                       cudaStream_t s, int* rc) {
+  const size_t bpp = sizeof(T);
+  if (((uintptr_t)d_in & 15) || ((uintptr_t)d_out & 15)) return false;
+  if ((g.in_pitch * bpp) % 16 || (g.out_pitch * bpp) % 16) return false;
+  if ((g.in_frame_stride * bpp) % 16 || (g.out_frame_stride * bpp) % 16) return false;
+  if (g.width < 16 || g.height < 1) return false;
+  bool taken = false;
+  int e = 0;
+  switch (k) {
+    case 3: e = launch_tile<T, 3>(d_in, d_out, g, method, counts, s, &taken); break;
+    case 5: e = launch_tile<T, 5>(d_in, d_out, g, method, counts, s, &taken); break;
+    case 7: e = launch_tile<T, 7>(d_in, d_out, g, method, counts, s, &taken); break;
+    case 9: e = launch_tile<T, 9>(d_in, d_out, g, method, counts, s, &taken); break;
+    case 11: e = launch_tile<T, 11>(d_in, d_out, g, method, counts, s, &taken); break;
+    default: return false;
+  }
+  if (!taken) return false;
+  *rc = e ? 2 : 0;
+  return true;
 }
 
 }  // namespace fast
