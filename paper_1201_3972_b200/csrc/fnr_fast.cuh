@@ -79,11 +79,22 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   if (!make_map<T>(&out_map, d_out, g.width, out_rows, g.batch, g.out_pitch, g.out_frame_stride, tile::TW,
                    tile::TH))
     return 0;
-  static bool attr_done = false;
-  if (!attr_done) {
+  // persistent grid: as many CTAs as fit on the device at once (cached per kernel)
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
     cudaFuncSetAttribute(tile::fnr_tile_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    attr_done = true;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tile::fnr_tile_kernel<T, K>, tile::THREADS, G::SMEM) !=
+            cudaSuccess ||
+        n < 1) {
+      cudaGetLastError();
+      n = 1;
+    }
+    blocks_per_sm = n;
   }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   tile::TileParams p;
   p.width = g.width;
   p.height = g.height;
@@ -95,9 +106,9 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.batch = g.batch;
   p.method = method;
   p.counts = counts;
-  const long long ntiles = (long long)p.tiles_x * p.tiles_y;
+  const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
-  dim3 grid((unsigned)ntiles, (unsigned)std::min<int>(g.batch, 65535));
+  dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));
   *taken = true;
   tile::fnr_tile_kernel<T, K><<<grid, tile::THREADS, G::SMEM, s>>>(in_map, out_map, p);
   cudaError_t e = cudaGetLastError();

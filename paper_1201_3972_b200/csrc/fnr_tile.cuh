@@ -1,20 +1,23 @@
-// TMA tile kernel for the FNR / MF pass (sm_100a).
+// TMA tile kernel for the FNR / MF pass (sm_100a), persistent and double-buffered.
 //
-// One CTA filters a TH x TW output tile of one frame:
-//   1. TMA (cp.async.bulk.tensor.3d) stages the (TH+2r) x BOXW input tile, halo
-//      included, into shared memory; TMA fills out-of-image cells with zeros,
-//      so tiles touching the frame border rewrite those cells from the nearest
-//      in-image cell (replicate edge, reference image.py:117-130).
+// Each CTA loops over TH x TW output tiles (tile t, t + gridDim.x, ...) of a
+// [batch, rows, width] u8/u16 image stack:
+//   1. TMA (cp.async.bulk.tensor.3d) stages the tile plus its halo into one of
+//      two shared-memory stages; the load of tile i+1 is in flight while tile i
+//      is filtered. TMA fills out-of-frame cells with zeros, so tiles touching
+//      the frame border rewrite those cells from the nearest in-frame cell
+//      (replicate edge, reference image.py:117-130).
 //   2. Detector (filters.py:169-171): separable window min/max on packed u16x2
-//      words (two horizontally adjacent pixels per 32-bit lane op): per input
-//      row a horizontal K-wide min/max, then a vertical K-row min/max over a
-//      register ring. A pixel is noisy iff centre == min or == max. Signal
-//      pixels are copied to the output tile; noisy pixels are compacted into a
-//      shared-memory queue with warp ballots.
+//      words (two horizontally adjacent pixels per 32-bit op): per input row a
+//      horizontal K-wide min/max, then a vertical K-row min/max over a register
+//      ring while each thread walks down its column pair. A pixel is noisy iff
+//      centre == min or == max. Signal pixels go straight to the output tile;
+//      noisy pixels set bits in a per-thread mask that is compacted into a
+//      shared-memory queue with one warp scan and one atomic per warp.
 //   3. Median (filters.py:172-176, sorting.py:51-56): each thread takes two
 //      queued pixels, packs their K*K window values into u16x2 words and runs
 //      one exact median-selection network (select_nets.cuh) for both.
-//      MF (filters.py:179-180) queues every pixel.
+//      MF (filters.py:179-180) runs the network on every pixel.
 //   4. The output tile leaves through a TMA store (clipped at the frame edge);
 //      detected / replacement counters go out with one atomic per CTA.
 #pragma once
@@ -26,10 +29,12 @@ namespace irdn {
 namespace tile {
 
 constexpr int THREADS = 256;
-constexpr int TW = 128;  // output tile width (pixels)
-constexpr int TH = 32;   // output tile height (rows)
-constexpr int BANDS = THREADS / (TW / 2);  // row bands in the detector
-constexpr int BAND_ROWS = TH / BANDS;
+constexpr int WARPS = THREADS / 32;
+constexpr int TW = 128;                 // output tile width (pixels) = 2 warps x 32 pairs
+constexpr int TH = 64;                  // output tile height (rows)
+constexpr int BANDS = WARPS / 2;        // row bands per tile
+constexpr int BAND = TH / BANDS;        // rows walked by one thread (<= 16: one flag bit per row and lane)
+static_assert(BAND <= 16, "flag mask holds 16 rows");
 
 template <typename T, int K>
 struct Geo {
@@ -45,11 +50,12 @@ struct Geo {
   static constexpr int BOXW = ((TW + R + r + ALIGN - 1) / ALIGN) * ALIGN;
   static constexpr int BOXH = TH + 2 * r;
   static constexpr int IN_BYTES = BOXW * BOXH * (int)sizeof(T);
+  static constexpr int IN_STRIDE = (IN_BYTES + 127) & ~127;
   static constexpr int OUT_BYTES = TW * TH * (int)sizeof(T);
-  static constexpr int IN_OFF = 0;
-  static constexpr int OUT_OFF = (IN_BYTES + 127) & ~127;
+  static constexpr int OUT_OFF = 2 * IN_STRIDE;
   static constexpr int Q_OFF = (OUT_OFF + OUT_BYTES + 127) & ~127;
-  static constexpr int SMEM = Q_OFF + TW * TH * 4 + 64 + 128;  // +128: runtime base alignment
+  static constexpr int BAR_OFF = Q_OFF + TW * TH * 2;
+  static constexpr int SMEM = BAR_OFF + 64 + 128;  // +128: runtime base alignment
   static_assert(BOXW <= 256 && BOXH <= 256, "TMA box limit");
 };
 
@@ -102,8 +108,11 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void tma_store_wait() {
+__device__ __forceinline__ void tma_store_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -142,83 +151,109 @@ __device__ __forceinline__ uint32_t median_dispatch(uint32_t (&v)[NV]) {
   else return median_net_121(v);
 }
 
+// Replicate-edge fix-up of the smem cells of a box that fall outside the frame.
+template <typename T, int K>
+__device__ __forceinline__ void fix_edges(T* s_in, int gx_lo, int gy_lo, int width, int height) {
+  using G = Geo<T, K>;
+  constexpr int BOXW = G::BOXW, BOXH = G::BOXH;
+  const int tid = threadIdx.x;
+  const int c_lo = max(0, -gx_lo), c_hi = min(BOXW, width - gx_lo);   // in-frame columns
+  const int y_lo = max(0, -gy_lo), y_hi = min(BOXH, height - gy_lo);  // in-frame rows
+  const int ncl = c_lo, ncr = BOXW - c_hi;
+  const int nc = ncl + ncr;
+  if (nc) {  // (a) left / right margins of in-frame rows
+    for (int i = tid; i < (y_hi - y_lo) * nc; i += THREADS) {
+      const int row = y_lo + i / nc;
+      const int j = i % nc;
+      const int col = j < ncl ? j : c_hi + (j - ncl);
+      s_in[row * BOXW + col] = s_in[row * BOXW + (j < ncl ? c_lo : c_hi - 1)];
+    }
+    __syncthreads();
+  }
+  const int nrt = y_lo, nrb = BOXH - y_hi;
+  // (b) rows above / below the frame copy the nearest in-frame row (corners included)
+  for (int i = tid; i < (nrt + nrb) * BOXW; i += THREADS) {
+    const int j = i / BOXW, col = i % BOXW;
+    const int row = j < nrt ? j : y_hi + (j - nrt);
+    s_in[row * BOXW + col] = s_in[(j < nrt ? y_lo : y_hi - 1) * BOXW + col];
+  }
+}
+
 // ---- the kernel ----------------------------------------------------------------
 template <typename T, int K>
 __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant__ CUtensorMap in_map,
                                                            const __grid_constant__ CUtensorMap out_map,
                                                            const TileParams p) {
   using G = Geo<T, K>;
-  constexpr int r = G::r, R = G::R, BOXW = G::BOXW, BOXH = G::BOXH;
+  constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   // TMA needs 128-byte aligned shared-memory boxes: align the dynamic base explicitly.
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  T* s_in = reinterpret_cast<T*>(smem + G::IN_OFF);
   T* s_out = reinterpret_cast<T*>(smem + G::OUT_OFF);
-  uint32_t* s_q = reinterpret_cast<uint32_t*>(smem + G::Q_OFF);
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + G::Q_OFF + TW * TH * 4);
-  int* s_qn = reinterpret_cast<int*>(smem + G::Q_OFF + TW * TH * 4 + 8);
+  uint16_t* s_q = reinterpret_cast<uint16_t*>(smem + G::Q_OFF);
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + G::BAR_OFF);  // [2] full barriers
+  int* s_qn = reinterpret_cast<int*>(smem + G::BAR_OFF + 16);
 
   const int tid = threadIdx.x;
-  const int tile = blockIdx.x;
-  const int tx0 = (tile % p.tiles_x) * TW;                  // output tile origin (frame coords)
-  const int ty0 = p.row_begin + (tile / p.tiles_x) * TH;    // global row
-  uint32_t replaced = 0;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int tiles_per_frame = p.tiles_x * p.tiles_y;
+  const int ntiles = tiles_per_frame * p.batch;
+  uint32_t replaced = 0, detected = 0;
+
+  auto tile_origin = [&](int t, int& b, int& tx0, int& ty0) {
+    b = t / tiles_per_frame;
+    const int tt = t - b * tiles_per_frame;
+    const int ty = tt / p.tiles_x;
+    tx0 = (tt - ty * p.tiles_x) * TW;
+    ty0 = p.row_begin + ty * TH;
+  };
+  auto issue_load = [&](int t, int stage) {
+    int b, tx0, ty0;
+    tile_origin(t, b, tx0, ty0);
+    mbar_expect_tx(&s_bar[stage], G::IN_BYTES);
+    tma_load_3d(smem + stage * G::IN_STRIDE, &in_map, &s_bar[stage], tx0 - R, ty0 - r - p.in_row0, b);
+  };
 
   if (tid == 0) {
-    mbar_init(s_bar, 1);
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
     *s_qn = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int t0 = blockIdx.x, t1 = blockIdx.x + gridDim.x;
+    if (t0 < ntiles) issue_load(t0, 0);
+    if (t1 < ntiles) issue_load(t1, 1);
   }
   __syncthreads();
 
-  for (int b = blockIdx.y; b < p.batch; b += gridDim.y) {
-    const int phase = ((b - (int)blockIdx.y) / (int)gridDim.y) & 1;
-    if (tid == 0) {
-      mbar_expect_tx(s_bar, G::IN_BYTES);
-      tma_load_3d(s_in, &in_map, s_bar, tx0 - R, ty0 - r - p.in_row0, b);
-    }
-    mbar_wait(s_bar, phase);
+  // detector geometry: warp -> (column half, row band); thread -> one column pair
+  const int w = (warp & 1) * 32 + lane;  // pair index: pixels 2w, 2w+1 of the tile row
+  const int band0 = (warp >> 1) * BAND;  // first output row of this thread's band
+  const int c0 = 2 * w + R;              // smem column of lane 0's pixel
 
-    // ---- replicate-edge fix-up of cells outside the frame ----
+  int iter = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
+    const int stage = iter & 1;
+    T* s_in = reinterpret_cast<T*>(smem + stage * G::IN_STRIDE);
+    int b, tx0, ty0;
+    tile_origin(t, b, tx0, ty0);
+    mbar_wait(&s_bar[stage], (iter >> 1) & 1);
     const int gx_lo = tx0 - R, gy_lo = ty0 - r;  // global coords of smem (0, 0)
-    const bool edge = gx_lo < 0 || gy_lo < 0 || gx_lo + BOXW > p.width || gy_lo + BOXH > p.height;
-    if (edge) {
-      const int c_lo = max(0, -gx_lo), c_hi = min(BOXW, p.width - gx_lo);     // in-frame columns
-      const int y_lo = max(0, -gy_lo), y_hi = min(BOXH, p.height - gy_lo);    // in-frame rows
-      const int ncl = c_lo, ncr = BOXW - c_hi;
-      // (a) left / right margins of in-frame rows
-      for (int i = tid; i < (y_hi - y_lo) * (ncl + ncr); i += THREADS) {
-        const int row = y_lo + i / (ncl + ncr);
-        const int j = i % (ncl + ncr);
-        const int col = j < ncl ? j : c_hi + (j - ncl);
-        s_in[row * BOXW + col] = s_in[row * BOXW + (j < ncl ? c_lo : c_hi - 1)];
-      }
-      __syncthreads();
-      // (b) rows above / below the frame copy the nearest in-frame row (corners included)
-      const int nrt = y_lo, nrb = BOXH - y_hi;
-      for (int i = tid; i < (nrt + nrb) * BOXW; i += THREADS) {
-        const int j = i / BOXW, col = i % BOXW;
-        const int row = j < nrt ? j : y_hi + (j - nrt);
-        s_in[row * BOXW + col] = s_in[(j < nrt ? y_lo : y_hi - 1) * BOXW + col];
-      }
-    }
+    if (gx_lo < 0 || gy_lo < 0 || gx_lo + BOXW > p.width || gy_lo + G::BOXH > p.height)
+      fix_edges<T, K>(s_in, gx_lo, gy_lo, p.width, p.height);
+    if (tid == 0) tma_store_wait_read();  // the previous tile's store has left s_out
     __syncthreads();
 
-    const int valid_w = min(TW, p.width - tx0);      // valid output columns in this tile
-    const int valid_h = min(TH, p.row_end - ty0);    // valid output rows
+    const int valid_w = min(TW, p.width - tx0);    // valid output columns in this tile
+    const int valid_h = min(TH, p.row_end - ty0);  // valid output rows
 
     if (p.method == 0) {
-      // ---- detector: separable min/max, packed pairs (lanes = columns 2w, 2w+1) ----
-      const int w = tid % (TW / 2);
-      const int band = tid / (TW / 2);
-      const int c0 = 2 * w + R;  // smem column of lane 0's pixel
+      // ---- detector ----
       constexpr int J = (r + 1) / 2;
-      uint32_t rmin[K], rmax[K];
-      const unsigned lane = tid & 31;
-      const unsigned lt_mask = (1u << lane) - 1u;
+      uint32_t rmin[K], rmax[K], rcen[r + 1];
+      uint32_t flags = 0;
 #pragma unroll
-      for (int s = 0; s < BAND_ROWS + 2 * r; ++s) {
-        const T* row = s_in + (band * BAND_ROWS + s) * BOXW;
+      for (int s = 0; s < BAND + 2 * r; ++s) {
+        const T* row = s_in + (band0 + s) * BOXW;
         uint32_t wd[2 * J + 1];
 #pragma unroll
         for (int j = -J; j <= J; ++j) wd[j + J] = load_pair<T>(row, c0 + 2 * j);
@@ -234,50 +269,64 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
         }
         rmin[s % K] = mn;
         rmax[s % K] = mx;
+        rcen[s % (r + 1)] = wd[J];
         if (s >= 2 * r) {
-          const int y = band * BAND_ROWS + s - 2 * r;  // output row in tile
+          const int y = s - 2 * r;  // output row within the band
           uint32_t vmn = rmin[0], vmx = rmax[0];
 #pragma unroll
           for (int i = 1; i < K; ++i) {
             vmn = vmin2(vmn, rmin[i]);
             vmx = vmax2(vmx, rmax[i]);
           }
-          const uint32_t c = load_pair<T>(s_in + (y + r) * BOXW, c0);
-          const uint32_t m = vmin2(c - vmn, vmx - c);  // lane == 0  <=>  centre is an extremum
-          const bool ok_row = y < valid_h;
-          const bool f0 = ok_row && (2 * w < valid_w) && (m & 0xFFFFu) == 0u;
-          const bool f1 = ok_row && (2 * w + 1 < valid_w) && (m >> 16) == 0u;
-          store_pair<T>(s_out + y * TW, 2 * w, c);
-          const unsigned b0 = __ballot_sync(0xffffffffu, f0);
-          const unsigned b1 = __ballot_sync(0xffffffffu, f1);
-          const int nq = __popc(b0) + __popc(b1);
-          if (nq) {
-            int base = 0;
-            if (lane == 0) base = atomicAdd(s_qn, nq);
-            base = __shfl_sync(0xffffffffu, base, 0);
-            int pos = base + __popc(b0 & lt_mask) + __popc(b1 & lt_mask);
-            const uint32_t e = ((uint32_t)y << 16) | (uint32_t)(2 * w);
-            if (f0) s_q[pos++] = e;
-            if (f1) s_q[pos] = e + 1u;
-          }
+          const uint32_t c = rcen[(s - r) % (r + 1)];
+          // lane of m == 0  <=>  centre equals the window min or max (no borrow: vmn <= c <= vmx)
+          const uint32_t m = vmin2(c - vmn, vmx - c);
+          // m < 0x8000 per lane (it is at most (max-min)/2), so +0x7FFF sets bit 15 iff m != 0
+          const uint32_t e = m + 0x7FFF7FFFu;
+          flags |= (~e & 0x80008000u) >> (15 - y);
+          store_pair<T>(s_out + (band0 + y) * TW, 2 * w, c);
         }
+      }
+      // mask out pixels beyond the frame / strip, then compact into the queue
+      const int vr = min(BAND, max(0, valid_h - band0));
+      const uint32_t rowm = vr >= 16 ? 0xFFFFu : ((1u << vr) - 1u);
+      const uint32_t colm = (2 * w < valid_w ? rowm : 0u) | (2 * w + 1 < valid_w ? (rowm << 16) : 0u);
+      flags &= colm;
+      const int cnt = __popc(flags);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      int base = 0;
+      if (lane == 31 && total) base = atomicAdd(s_qn, total);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      int pos = base + incl - cnt;
+      while (flags) {
+        const int bit = __ffs(flags) - 1;
+        flags &= flags - 1u;
+        const int y = band0 + (bit & 15);
+        s_q[pos++] = (uint16_t)((y << 8) | (2 * w + (bit >> 4)));
       }
       __syncthreads();
     }
 
     // ---- median of queued (FNR) or all (MF) pixels, two per thread ----
     const int n = p.method == 0 ? *s_qn : TW * TH;
+    if (p.method == 0) detected += (tid == 0) ? (uint32_t)n : 0u;
     for (int i = tid; 2 * i < n; i += THREADS) {
       uint32_t e0, e1;
       if (p.method == 0) {
         e0 = s_q[2 * i];
         e1 = (2 * i + 1 < n) ? s_q[2 * i + 1] : e0;
       } else {
-        e0 = ((uint32_t)((2 * i) / TW) << 16) | (uint32_t)((2 * i) % TW);
+        e0 = ((uint32_t)((2 * i) / TW) << 8) | (uint32_t)((2 * i) % TW);
         e1 = e0 + 1u;
       }
-      const int y0 = (int)(e0 >> 16), x0 = (int)(e0 & 0xFFFFu);
-      const int y1 = (int)(e1 >> 16), x1 = (int)(e1 & 0xFFFFu);
+      const int y0 = (int)(e0 >> 8), x0 = (int)(e0 & 0xFFu);
+      const int y1 = (int)(e1 >> 8), x1 = (int)(e1 & 0xFFu);
       const T* a = s_in + y0 * BOXW + x0 + (R - r);
       const T* bb = s_in + y1 * BOXW + x1 + (R - r);
       uint32_t v[K * K];
@@ -303,13 +352,13 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
     __syncthreads();
     if (tid == 0) {
       tma_store_3d(&out_map, s_out, tx0, ty0 - p.row_begin, b);
-      if (p.method == 0 && *s_qn) atomicAdd(&p.counts[0], (unsigned long long)*s_qn);
       *s_qn = 0;
-      tma_store_wait();  // the next frame overwrites s_out
+      const int tn = t + 2 * gridDim.x;  // this stage is free again: prefetch two tiles ahead
+      if (tn < ntiles) issue_load(tn, stage);
     }
-    __syncthreads();
   }
-  if (p.method == 0) block_add_counts<THREADS>(0u, replaced, p.counts);
+  if (tid == 0) tma_store_wait_all();
+  if (p.method == 0) block_add_counts<THREADS>(detected, replaced, p.counts);
 }
 
 }  // namespace tile

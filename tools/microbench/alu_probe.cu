@@ -39,6 +39,11 @@ __global__ void alu_kernel(uint32_t* out, uint32_t seed) {
       if (OP == 4) asm volatile("prmt.b32 %0, %0, %1, 0x5410;" : "+r"(v[i]) : "r"(b));  // PRMT
       if (OP == 5) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(v[i]) : "r"(b), "r"(c));  // LOP3
       if (OP == 6) { uint32_t t = min3(v[i], b, c); v[i] = max3(t, b, c); }  // mixed min/max pair
+      if (OP == 8) { uint32_t t; asm volatile("min.f16x2 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // HMNMX2
+      if (OP == 9) { uint32_t t; asm volatile("min.bf16x2 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // bf16 min
+      if (OP == 10) { uint32_t t; if (i & 1) asm volatile("min.f16x2 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); else asm volatile("min.u16x2 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // mixed
+      if (OP == 11) { uint32_t t; asm volatile("min.f32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // FMNMX
+      if (OP == 12) { uint32_t t; if (i & 1) asm volatile("add.u32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); else asm volatile("min.u16x2 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // VIMNMX + IADD mix
       if (OP == 7) { uint32_t t; asm volatile("min.u32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // IMNMX.U32
     }
   }
@@ -91,6 +96,11 @@ int main() {
   run_alu<5>("lop3", 1);
   run_alu<6>("vimnmx3_minmax_pair", 2);
   run_alu<7>("imnmx_u32", 1);
+  run_alu<8>("hmnmx2_f16x2", 1);
+  run_alu<9>("hmnmx2_bf16x2", 1);
+  run_alu<10>("mixed_vimnmx_hmnmx2", 1);
+  run_alu<11>("fmnmx_f32", 1);
+  run_alu<12>("mixed_vimnmx_iadd", 1);
 
   // HBM copy: 2 GiB in + 2 GiB out
   size_t bytes = (size_t)2 << 30;
