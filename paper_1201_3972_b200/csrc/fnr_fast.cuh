@@ -67,17 +67,38 @@ inline bool make_map(CUtensorMap* map, const void* base, int64_t width, int64_t 
   return true;
 }
 
+// Per-device pool of tile-scheduler slots ({next tile, finished CTAs}, 128 B apart).
+// Each launch takes the next slot round-robin; a slot returns to {0, 0} when the
+// launch using it finishes, so up to kSlots launches may be in flight at once.
+constexpr int kSchedSlots = 256;
+inline unsigned int* sched_slot(int dev) {
+  static std::mutex mu;
+  static unsigned int* pool[64] = {nullptr};
+  static unsigned int next[64] = {0};
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pool[dev]) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, (size_t)kSchedSlots * 128) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    cudaMemset(p, 0, (size_t)kSchedSlots * 128);
+    cudaDeviceSynchronize();
+    pool[dev] = static_cast<unsigned int*>(p);
+  }
+  const unsigned int slot = next[dev]++ % kSchedSlots;
+  return pool[dev] + slot * 32;
+}
+
 template <typename T, int K>
 inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, unsigned long long* counts,
                        cudaStream_t s, bool* taken) {
   using G = tile::Geo<T, K>;
   *taken = false;
-  CUtensorMap in_map, out_map;
+  CUtensorMap in_map;
   const int out_rows = g.row_end - g.row_begin;
   if (!make_map<T>(&in_map, d_in, g.width, g.in_rows, g.batch, g.in_pitch, g.in_frame_stride, G::BOXW, G::BOXH))
-    return 0;
-  if (!make_map<T>(&out_map, d_out, g.width, out_rows, g.batch, g.out_pitch, g.out_frame_stride, tile::TW,
-                   tile::TH))
     return 0;
   // persistent grid: as many CTAs as fit on the device at once (cached per kernel)
   static int blocks_per_sm = 0;
@@ -95,7 +116,12 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  unsigned int* sched = sched_slot(dev);
+  if (!sched) return 0;
   tile::TileParams p;
+  p.out = d_out;
+  p.out_pitch = g.out_pitch;
+  p.out_frame = g.out_frame_stride;
   p.width = g.width;
   p.height = g.height;
   p.in_row0 = g.in_row0;
@@ -106,11 +132,12 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.batch = g.batch;
   p.method = method;
   p.counts = counts;
+  p.sched = sched;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));
   *taken = true;
-  tile::fnr_tile_kernel<T, K><<<grid, tile::THREADS, G::SMEM, s>>>(in_map, out_map, p);
+  tile::fnr_tile_kernel<T, K><<<grid, tile::THREADS, G::SMEM, s>>>(in_map, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_fast_err = cudaGetErrorString(e);

@@ -1,40 +1,45 @@
-// TMA tile kernel for the FNR / MF pass (sm_100a), persistent and double-buffered.
+// TMA tile kernel for the FNR / MF pass (sm_100a): persistent, per-warp work queues.
 //
-// Each CTA loops over TH x TW output tiles (tile t, t + gridDim.x, ...) of a
+// Each CTA (4 warps) loops over TH x TW output tiles (t, t + gridDim.x, ...) of a
 // [batch, rows, width] u8/u16 image stack:
 //   1. TMA (cp.async.bulk.tensor.3d) stages the tile plus its halo into one of
-//      two shared-memory stages; the load of tile i+1 is in flight while tile i
-//      is filtered. TMA fills out-of-frame cells with zeros, so tiles touching
-//      the frame border rewrite those cells from the nearest in-frame cell
-//      (replicate edge, reference image.py:117-130).
-//   2. Detector (filters.py:169-171): separable window min/max on packed u16x2
-//      words (two horizontally adjacent pixels per 32-bit op): per input row a
-//      horizontal K-wide min/max, then a vertical K-row min/max over a register
-//      ring while each thread walks down its column pair. A pixel is noisy iff
-//      centre == min or == max. Signal pixels go straight to the output tile;
-//      noisy pixels set bits in a per-thread mask that is compacted into a
-//      shared-memory queue with one warp scan and one atomic per warp.
-//   3. Median (filters.py:172-176, sorting.py:51-56): each thread takes two
-//      queued pixels, packs their K*K window values into u16x2 words and runs
-//      one exact median-selection network (select_nets.cuh) for both.
+//      NSTAGE shared-memory stages; with two stages the load of the next tile is
+//      in flight while this one is filtered. TMA fills out-of-frame cells with
+//      zeros, so tiles touching the frame border rewrite those cells from the
+//      nearest in-frame cell (replicate edge, reference image.py:117-130).
+//   2. Detector (filters.py:169-171): each warp owns a 64 x 32 strip; each thread
+//      one column pair (two horizontally adjacent pixels packed as u16x2) walking
+//      down the strip. Per input row a horizontal K-wide min/max, then a vertical
+//      K-row min/max over a register ring. A pixel is noisy iff centre == min or
+//      == max. Signal pixels are stored straight to global memory (one coalesced
+//      128-byte row segment per warp); noisy pixels set bits in per-thread masks.
+//   3. Median (filters.py:172-176, sorting.py:51-56): per 16-row half strip, the
+//      warp compacts its noisy pixels into a warp-private queue (one warp scan),
+//      then each lane takes two queued pixels, packs their K*K window values into
+//      u16x2 words and runs one exact median-selection network (select_nets.cuh)
+//      for both; medians overwrite the copied centres in global memory.
 //      MF (filters.py:179-180) runs the network on every pixel.
-//   4. The output tile leaves through a TMA store (clipped at the frame edge);
-//      detected / replacement counters go out with one atomic per CTA.
+//   4. Detected / replacement counters leave with one atomic per CTA at the end.
 #pragma once
 #include <cuda.h>
 #include "fnr_common.cuh"
 #include "select_nets.cuh"
 
+#ifndef IRDN_NSTAGE
+#define IRDN_NSTAGE 1
+#endif
+
 namespace irdn {
 namespace tile {
 
-constexpr int THREADS = 256;
+constexpr int THREADS = 128;
 constexpr int WARPS = THREADS / 32;
-constexpr int TW = 128;                 // output tile width (pixels) = 2 warps x 32 pairs
+constexpr int TW = 128;                 // output tile width (pixels) = 2 warps x 32 pixel pairs
 constexpr int TH = 64;                  // output tile height (rows)
-constexpr int BANDS = WARPS / 2;        // row bands per tile
-constexpr int BAND = TH / BANDS;        // rows walked by one thread (<= 16: one flag bit per row and lane)
-static_assert(BAND <= 16, "flag mask holds 16 rows");
+constexpr int BAND = TH / (WARPS / 2);  // rows walked by one thread (two 16-row flag words)
+constexpr int STRIP_PX = 64 * BAND;     // pixels of one warp strip (queue capacity)
+constexpr int NSTAGE = IRDN_NSTAGE;     // input stages (2 = double-buffered TMA)
+static_assert(BAND == 32, "two 16-row flag words per thread");
 
 template <typename T, int K>
 struct Geo {
@@ -51,25 +56,28 @@ struct Geo {
   static constexpr int BOXH = TH + 2 * r;
   static constexpr int IN_BYTES = BOXW * BOXH * (int)sizeof(T);
   static constexpr int IN_STRIDE = (IN_BYTES + 127) & ~127;
-  static constexpr int OUT_BYTES = TW * TH * (int)sizeof(T);
-  static constexpr int OUT_OFF = 2 * IN_STRIDE;
-  static constexpr int Q_OFF = (OUT_OFF + OUT_BYTES + 127) & ~127;
-  static constexpr int BAR_OFF = Q_OFF + TW * TH * 2;
-  static constexpr int SMEM = BAR_OFF + 64 + 128;  // +128: runtime base alignment
+  static constexpr int Q_OFF = NSTAGE * IN_STRIDE;
+  static constexpr int BAR_OFF = Q_OFF + WARPS * STRIP_PX * 2;
+  static constexpr int TILE_OFF = BAR_OFF + 8 * NSTAGE;  // tile id staged in each buffer
+  static constexpr int SMEM = TILE_OFF + 4 * NSTAGE + 128;  // +128: runtime base alignment
   static_assert(BOXW <= 256 && BOXH <= 256, "TMA box limit");
 };
 
 struct TileParams {
+  void* out;          // output pixel (row_begin, 0) of frame 0
+  int64_t out_pitch;  // elements
+  int64_t out_frame;  // elements between output frames
   int32_t width;      // frame width
   int32_t height;     // GLOBAL frame height (clamp bound)
   int32_t in_row0;    // global row of input-map row 0
-  int32_t row_begin;  // first output row (global); output-map row 0
+  int32_t row_begin;  // first output row (global)
   int32_t row_end;
   int32_t tiles_x;
   int32_t tiles_y;
   int32_t batch;
   int32_t method;     // 0 fnr, 1 mf
   unsigned long long* counts;
+  unsigned int* sched;  // [0] next tile to hand out, [1] finished CTAs (reset to 0 by the last CTA)
 };
 
 // ---- PTX helpers ------------------------------------------------------------
@@ -102,18 +110,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
-               "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void tma_store_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void tma_store_wait_all() {
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -133,12 +129,15 @@ __device__ __forceinline__ uint32_t load_pair(const T* row, int col) {
     return prmt(b, 0u, 0x4140u);  // bytes (b0, 0, b1, 0)
   }
 }
+// Store a packed pixel pair to global memory (lanes beyond the frame are dropped).
 template <typename T>
-__device__ __forceinline__ void store_pair(T* row, int col, uint32_t v) {
+__device__ __forceinline__ void store_pair_g(T* dst, uint32_t v, bool ok0, bool ok1) {
   if constexpr (sizeof(T) == 2) {
-    *reinterpret_cast<uint32_t*>(row + col) = v;
+    if (ok0 && ok1) *reinterpret_cast<uint32_t*>(dst) = v;
+    else if (ok0) dst[0] = (T)(v & 0xFFFFu);
   } else {
-    *reinterpret_cast<uint16_t*>(row + col) = (uint16_t)prmt(v, 0u, 0x0020u);
+    if (ok0 && ok1) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)prmt(v, 0u, 0x0020u);
+    else if (ok0) dst[0] = (T)(v & 0xFFu);
   }
 }
 
@@ -151,6 +150,26 @@ __device__ __forceinline__ uint32_t median_dispatch(uint32_t (&v)[NV]) {
   else return median_net_121(v);
 }
 
+// Min / max of N packed words with 3-input VIMNMX3 (N odd: (N-1)/2 instructions).
+template <int N>
+__device__ __forceinline__ uint32_t reduce_min(const uint32_t (&a)[N]) {
+  uint32_t m = a[0];
+  int i = 1;
+#pragma unroll
+  for (; i + 1 < N; i += 2) m = vmin3(m, a[i], a[i + 1]);
+  if (i < N) m = vmin2(m, a[i]);
+  return m;
+}
+template <int N>
+__device__ __forceinline__ uint32_t reduce_max(const uint32_t (&a)[N]) {
+  uint32_t m = a[0];
+  int i = 1;
+#pragma unroll
+  for (; i + 1 < N; i += 2) m = vmax3(m, a[i], a[i + 1]);
+  if (i < N) m = vmax2(m, a[i]);
+  return m;
+}
+
 // Replicate-edge fix-up of the smem cells of a box that fall outside the frame.
 template <typename T, int K>
 __device__ __forceinline__ void fix_edges(T* s_in, int gx_lo, int gy_lo, int width, int height) {
@@ -161,41 +180,71 @@ __device__ __forceinline__ void fix_edges(T* s_in, int gx_lo, int gy_lo, int wid
   const int y_lo = max(0, -gy_lo), y_hi = min(BOXH, height - gy_lo);  // in-frame rows
   const int ncl = c_lo, ncr = BOXW - c_hi;
   const int nc = ncl + ncr;
-  if (nc) {  // (a) left / right margins of in-frame rows
-    for (int i = tid; i < (y_hi - y_lo) * nc; i += THREADS) {
-      const int row = y_lo + i / nc;
-      const int j = i % nc;
-      const int col = j < ncl ? j : c_hi + (j - ncl);
-      s_in[row * BOXW + col] = s_in[row * BOXW + (j < ncl ? c_lo : c_hi - 1)];
+  const int lane = tid & 31, warp = tid >> 5;
+  if (nc) {  // (a) left / right margins of in-frame rows: warps over rows, lanes over columns
+    for (int row = y_lo + warp; row < y_hi; row += WARPS) {
+      T* rp = s_in + row * BOXW;
+      for (int j = lane; j < nc; j += 32) {
+        const int col = j < ncl ? j : c_hi + (j - ncl);
+        rp[col] = rp[j < ncl ? c_lo : c_hi - 1];
+      }
     }
     __syncthreads();
   }
   const int nrt = y_lo, nrb = BOXH - y_hi;
   // (b) rows above / below the frame copy the nearest in-frame row (corners included)
-  for (int i = tid; i < (nrt + nrb) * BOXW; i += THREADS) {
-    const int j = i / BOXW, col = i % BOXW;
-    const int row = j < nrt ? j : y_hi + (j - nrt);
-    s_in[row * BOXW + col] = s_in[(j < nrt ? y_lo : y_hi - 1) * BOXW + col];
+  for (int j = warp; j < nrt + nrb; j += WARPS) {
+    T* rp = s_in + (j < nrt ? j : y_hi + (j - nrt)) * BOXW;
+    const T* src = s_in + (j < nrt ? y_lo : y_hi - 1) * BOXW;
+    for (int col = lane; col < BOXW; col += 32) rp[col] = src[col];
   }
+}
+
+// Median of the pixels listed in q[0..n) (tile coords y << 8 | x), two per lane; the
+// medians overwrite the copied centres at out_tile. Returns this lane's replacements.
+template <typename T, int K>
+__device__ __forceinline__ uint32_t median_queue(const T* s_in, const uint16_t* q, int n, T* out_tile,
+                                                 int64_t pitch, int lane, bool fnr) {
+  using G = Geo<T, K>;
+  constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
+  uint32_t replaced = 0;
+  for (int i = lane; 2 * i < n; i += 32) {
+    const uint32_t e0 = q[2 * i];
+    const bool two = 2 * i + 1 < n;
+    const uint32_t e1 = two ? q[2 * i + 1] : e0;
+    const int y0 = (int)(e0 >> 8), x0 = (int)(e0 & 0xFFu);
+    const int y1 = (int)(e1 >> 8), x1 = (int)(e1 & 0xFFu);
+    const T* a = s_in + y0 * BOXW + x0 + (R - r);
+    const T* bb = s_in + y1 * BOXW + x1 + (R - r);
+    uint32_t v[K * K];
+#pragma unroll
+    for (int dy = 0; dy < K; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < K; ++dx)
+        v[dy * K + dx] = (uint32_t)a[dy * BOXW + dx] | ((uint32_t)bb[dy * BOXW + dx] << 16);
+    const uint32_t med = median_dispatch<K * K>(v);
+    const uint32_t m0 = med & 0xFFFFu, m1 = med >> 16;
+    out_tile[y0 * pitch + x0] = (T)m0;
+    if (two) out_tile[y1 * pitch + x1] = (T)m1;
+    if (fnr) replaced += (m0 != (uint32_t)a[r * BOXW + r]) + (two && m1 != (uint32_t)bb[r * BOXW + r]);
+  }
+  return replaced;
 }
 
 // ---- the kernel ----------------------------------------------------------------
 template <typename T, int K>
 __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant__ CUtensorMap in_map,
-                                                           const __grid_constant__ CUtensorMap out_map,
                                                            const TileParams p) {
   using G = Geo<T, K>;
   constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   // TMA needs 128-byte aligned shared-memory boxes: align the dynamic base explicitly.
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  T* s_out = reinterpret_cast<T*>(smem + G::OUT_OFF);
-  uint16_t* s_q = reinterpret_cast<uint16_t*>(smem + G::Q_OFF);
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + G::BAR_OFF);  // [2] full barriers
-  int* s_qn = reinterpret_cast<int*>(smem + G::BAR_OFF + 16);
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + G::BAR_OFF);  // [NSTAGE] stage-full barriers
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  uint16_t* s_q = reinterpret_cast<uint16_t*>(smem + G::Q_OFF) + warp * STRIP_PX;  // this warp's queue
   const int tiles_per_frame = p.tiles_x * p.tiles_y;
   const int ntiles = tiles_per_frame * p.batch;
   uint32_t replaced = 0, detected = 0;
@@ -207,157 +256,143 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
     tx0 = (tt - ty * p.tiles_x) * TW;
     ty0 = p.row_begin + ty * TH;
   };
-  auto issue_load = [&](int t, int stage) {
-    int b, tx0, ty0;
-    tile_origin(t, b, tx0, ty0);
-    mbar_expect_tx(&s_bar[stage], G::IN_BYTES);
-    tma_load_3d(smem + stage * G::IN_STRIDE, &in_map, &s_bar[stage], tx0 - R, ty0 - r - p.in_row0, b);
+  int* s_tile = reinterpret_cast<int*>(smem + G::TILE_OFF);
+  // Dynamic tile scheduler (thread 0): grab the next tile, publish its id next to the
+  // stage, then arrive on the stage barrier (with the TMA bytes, or empty past the end).
+  // The barrier's release/acquire makes the id visible to every waiting thread.
+  auto refill = [&](int stage) {
+    const int t = (int)atomicAdd(p.sched, 1u);
+    s_tile[stage] = t;
+    if (t < ntiles) {
+      int b, tx0, ty0;
+      tile_origin(t, b, tx0, ty0);
+      mbar_expect_tx(&s_bar[stage], G::IN_BYTES);
+      tma_load_3d(smem + stage * G::IN_STRIDE, &in_map, &s_bar[stage], tx0 - R, ty0 - r - p.in_row0, b);
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_bar[stage])) : "memory");
+    }
   };
 
   if (tid == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
-    *s_qn = 0;
+#pragma unroll
+    for (int s = 0; s < NSTAGE; ++s) mbar_init(&s_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const int t0 = blockIdx.x, t1 = blockIdx.x + gridDim.x;
-    if (t0 < ntiles) issue_load(t0, 0);
-    if (t1 < ntiles) issue_load(t1, 1);
+#pragma unroll
+    for (int s = 0; s < NSTAGE; ++s) refill(s);
   }
   __syncthreads();
 
-  // detector geometry: warp -> (column half, row band); thread -> one column pair
-  const int w = (warp & 1) * 32 + lane;  // pair index: pixels 2w, 2w+1 of the tile row
-  const int band0 = (warp >> 1) * BAND;  // first output row of this thread's band
-  const int c0 = 2 * w + R;              // smem column of lane 0's pixel
+  const int cpair = (warp & 1) * 32 + lane;  // pixel pair: tile columns 2*cpair, 2*cpair+1
+  const int band0 = (warp >> 1) * BAND;      // first tile row of this warp's strip
+  const int c0 = 2 * cpair + R;              // smem column of lane 0's pixel
+  T* const out_base = reinterpret_cast<T*>(p.out);
 
-  int iter = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
-    const int stage = iter & 1;
+  for (int iter = 0;; ++iter) {
+    const int stage = NSTAGE == 1 ? 0 : (iter % NSTAGE);
     T* s_in = reinterpret_cast<T*>(smem + stage * G::IN_STRIDE);
+    mbar_wait(&s_bar[stage], (iter / NSTAGE) & 1);
+    const int t = s_tile[stage];
+    if (t >= ntiles) break;
     int b, tx0, ty0;
     tile_origin(t, b, tx0, ty0);
-    mbar_wait(&s_bar[stage], (iter >> 1) & 1);
     const int gx_lo = tx0 - R, gy_lo = ty0 - r;  // global coords of smem (0, 0)
-    if (gx_lo < 0 || gy_lo < 0 || gx_lo + BOXW > p.width || gy_lo + G::BOXH > p.height)
+    if (gx_lo < 0 || gy_lo < 0 || gx_lo + BOXW > p.width || gy_lo + G::BOXH > p.height) {
       fix_edges<T, K>(s_in, gx_lo, gy_lo, p.width, p.height);
-    if (tid == 0) tma_store_wait_read();  // the previous tile's store has left s_out
-    __syncthreads();
+      __syncthreads();
+    }
 
     const int valid_w = min(TW, p.width - tx0);    // valid output columns in this tile
     const int valid_h = min(TH, p.row_end - ty0);  // valid output rows
+    T* const out_tile = out_base + (int64_t)b * p.out_frame + (int64_t)(ty0 - p.row_begin) * p.out_pitch + tx0;
+    const bool ok0 = 2 * cpair < valid_w, ok1 = 2 * cpair + 1 < valid_w;
 
     if (p.method == 0) {
-      // ---- detector ----
+      // ---- detector: horizontal K-wide min/max per input row, vertical K-row ring ----
       constexpr int J = (r + 1) / 2;
       uint32_t rmin[K], rmax[K], rcen[r + 1];
-      uint32_t flags = 0;
+      uint32_t flags[2] = {0u, 0u};
 #pragma unroll
       for (int s = 0; s < BAND + 2 * r; ++s) {
         const T* row = s_in + (band0 + s) * BOXW;
         uint32_t wd[2 * J + 1];
 #pragma unroll
         for (int j = -J; j <= J; ++j) wd[j + J] = load_pair<T>(row, c0 + 2 * j);
-        uint32_t mn = wd[J], mx = wd[J];
+        uint32_t ops[K];  // lane-aligned operands for horizontal offsets -r..r
 #pragma unroll
-        for (int d = -r; d <= r; ++d) {
-          if (d == 0) continue;
-          uint32_t op;
-          if ((d & 1) == 0) op = wd[J + d / 2];
-          else op = prmt(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], 0x5432u);
-          mn = vmin2(mn, op);
-          mx = vmax2(mx, op);
-        }
+        for (int d = -r; d <= r; ++d)
+          ops[d + r] = (d & 1) == 0 ? wd[J + d / 2] : prmt(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], 0x5432u);
+        const uint32_t mn = reduce_min<K>(ops), mx = reduce_max<K>(ops);
         rmin[s % K] = mn;
         rmax[s % K] = mx;
         rcen[s % (r + 1)] = wd[J];
         if (s >= 2 * r) {
-          const int y = s - 2 * r;  // output row within the band
-          uint32_t vmn = rmin[0], vmx = rmax[0];
-#pragma unroll
-          for (int i = 1; i < K; ++i) {
-            vmn = vmin2(vmn, rmin[i]);
-            vmx = vmax2(vmx, rmax[i]);
-          }
+          const int y = s - 2 * r;  // output row within the strip
+          const uint32_t vmn = reduce_min<K>(rmin), vmx = reduce_max<K>(rmax);
           const uint32_t c = rcen[(s - r) % (r + 1)];
           // lane of m == 0  <=>  centre equals the window min or max (no borrow: vmn <= c <= vmx)
           const uint32_t m = vmin2(c - vmn, vmx - c);
           // m < 0x8000 per lane (it is at most (max-min)/2), so +0x7FFF sets bit 15 iff m != 0
           const uint32_t e = m + 0x7FFF7FFFu;
-          flags |= (~e & 0x80008000u) >> (15 - y);
-          store_pair<T>(s_out + (band0 + y) * TW, 2 * w, c);
+          flags[y >> 4] |= (~e & 0x80008000u) >> (15 - (y & 15));
+          if (band0 + y < valid_h)
+            store_pair_g<T>(out_tile + (int64_t)(band0 + y) * p.out_pitch + 2 * cpair, c, ok0, ok1);
         }
       }
-      // mask out pixels beyond the frame / strip, then compact into the queue
+      // mask out pixels beyond the frame / strip, compact into the warp queue, median
+      const uint32_t colm = (ok0 ? 0xFFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
       const int vr = min(BAND, max(0, valid_h - band0));
-      const uint32_t rowm = vr >= 16 ? 0xFFFFu : ((1u << vr) - 1u);
-      const uint32_t colm = (2 * w < valid_w ? rowm : 0u) | (2 * w + 1 < valid_w ? (rowm << 16) : 0u);
-      flags &= colm;
-      const int cnt = __popc(flags);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int v = min(16, max(0, vr - 16 * h));
+        const uint32_t rowm = v >= 16 ? 0xFFFFu : ((1u << v) - 1u);
+        flags[h] &= colm & (rowm | (rowm << 16));
+      }
+      const int cnt = __popc(flags[0]) + __popc(flags[1]);
       int incl = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
       }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      int base = 0;
-      if (lane == 31 && total) base = atomicAdd(s_qn, total);
-      base = __shfl_sync(0xffffffffu, base, 31);
-      int pos = base + incl - cnt;
-      while (flags) {
-        const int bit = __ffs(flags) - 1;
-        flags &= flags - 1u;
-        const int y = band0 + (bit & 15);
-        s_q[pos++] = (uint16_t)((y << 8) | (2 * w + (bit >> 4)));
-      }
-      __syncthreads();
-    }
-
-    // ---- median of queued (FNR) or all (MF) pixels, two per thread ----
-    const int n = p.method == 0 ? *s_qn : TW * TH;
-    if (p.method == 0) detected += (tid == 0) ? (uint32_t)n : 0u;
-    for (int i = tid; 2 * i < n; i += THREADS) {
-      uint32_t e0, e1;
-      if (p.method == 0) {
-        e0 = s_q[2 * i];
-        e1 = (2 * i + 1 < n) ? s_q[2 * i + 1] : e0;
-      } else {
-        e0 = ((uint32_t)((2 * i) / TW) << 8) | (uint32_t)((2 * i) % TW);
-        e1 = e0 + 1u;
-      }
-      const int y0 = (int)(e0 >> 8), x0 = (int)(e0 & 0xFFu);
-      const int y1 = (int)(e1 >> 8), x1 = (int)(e1 & 0xFFu);
-      const T* a = s_in + y0 * BOXW + x0 + (R - r);
-      const T* bb = s_in + y1 * BOXW + x1 + (R - r);
-      uint32_t v[K * K];
+      const int n = __shfl_sync(0xffffffffu, incl, 31);
+      detected += (uint32_t)cnt;
+      int pos = incl - cnt;
 #pragma unroll
-      for (int dy = 0; dy < K; ++dy)
-#pragma unroll
-        for (int dx = 0; dx < K; ++dx)
-          v[dy * K + dx] = (uint32_t)a[dy * BOXW + dx] | ((uint32_t)bb[dy * BOXW + dx] << 16);
-      const uint32_t med = median_dispatch<K * K>(v);
-      const uint32_t m0 = med & 0xFFFFu, m1 = med >> 16;
-      s_out[y0 * TW + x0] = (T)m0;
-      if (p.method == 0) {
-        replaced += (m0 != (uint32_t)a[r * BOXW + r]);
-        if (2 * i + 1 < n) {
-          s_out[y1 * TW + x1] = (T)m1;
-          replaced += (m1 != (uint32_t)bb[r * BOXW + r]);
+      for (int h = 0; h < 2; ++h) {
+        uint32_t f = flags[h];
+        while (f) {
+          const int bit = __ffs(f) - 1;
+          f &= f - 1u;
+          const int y = band0 + 16 * h + (bit & 15);
+          s_q[pos++] = (uint16_t)((y << 8) | (2 * cpair + (bit >> 4)));
         }
-      } else {
-        s_out[y1 * TW + x1] = (T)m1;
       }
+      __syncwarp();  // queue visible; centre stores ordered before the median stores
+      replaced += median_queue<T, K>(s_in, s_q, n, out_tile, p.out_pitch, lane, true);
+      __syncwarp();
+    } else {
+      // MF: every valid pixel of the strip through the same queue
+      const int cols = max(0, min(64, valid_w - (warp & 1) * 64));
+      const int rows = min(BAND, max(0, valid_h - band0));
+      const int n = rows * cols;
+      for (int j = lane; j < n; j += 32) {
+        const int y = j / cols, x = j - y * cols;
+        s_q[j] = (uint16_t)(((band0 + y) << 8) | ((warp & 1) * 64 + x));
+      }
+      __syncwarp();
+      median_queue<T, K>(s_in, s_q, n, out_tile, p.out_pitch, lane, false);
+      __syncwarp();
     }
+    // all warps are done with this stage: refill it with the next tile
     fence_proxy_async();
     __syncthreads();
-    if (tid == 0) {
-      tma_store_3d(&out_map, s_out, tx0, ty0 - p.row_begin, b);
-      *s_qn = 0;
-      const int tn = t + 2 * gridDim.x;  // this stage is free again: prefetch two tiles ahead
-      if (tn < ntiles) issue_load(tn, stage);
-    }
+    if (tid == 0) refill(stage);
   }
-  if (tid == 0) tma_store_wait_all();
+  // the last CTA out resets the scheduler for the next launch on this slot
+  if (tid == 0 && atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+    p.sched[0] = 0u;
+    p.sched[1] = 0u;
+  }
   if (p.method == 0) block_add_counts<THREADS>(detected, replaced, p.counts);
 }
 

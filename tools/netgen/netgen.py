@@ -133,18 +133,96 @@ def check(n, ops, out_slot):
         assert evaluate(ops, out_slot, vals) == sorted(vals)[rank], f"random check failed n={n}"
 
 
-def emit(n, ops, out_slot) -> str:
-    lines = [f"// median of {n} values: {len(ops)} comparators, "
-             f"{sum(2 if o[0] == 'cx' else 1 for o in ops)} packed min/max ops",
-             f"__device__ __forceinline__ uint32_t median_net_{n}(uint32_t (&v)[{n}]) {{"]
+def to_ssa(n, ops, out_slot):
+    """Lower a slot network to SSA instructions and fuse single-use min->min / max->max
+    chains into 3-input min/max (VIMNMX3.U16x2 on sm_100a).
+
+    Returns (instrs, result) with instrs = [(name, kind, [srcs])], kind in min/max
+    (2 or 3 sources); sources are 'x<i>' inputs or earlier names."""
+    cur = [f"x{i}" for i in range(n)]
+    instrs = {}
+    order = []
+    cnt = 0
+
+    def new(kind, srcs):
+        nonlocal cnt
+        name = f"t{cnt}"
+        cnt += 1
+        instrs[name] = [kind, list(srcs)]
+        order.append(name)
+        return name
+
     for op, a, b in ops:
-        if op == "cx":
-            lines.append(f"  {{ const uint32_t t = vmin2(v[{a}], v[{b}]); v[{b}] = vmax2(v[{a}], v[{b}]); v[{a}] = t; }}")
-        elif op == "min":
-            lines.append(f"  v[{a}] = vmin2(v[{a}], v[{b}]);")
-        else:
-            lines.append(f"  v[{b}] = vmax2(v[{a}], v[{b}]);")
-    lines.append(f"  return v[{out_slot}];")
+        va, vb = cur[a], cur[b]
+        if op in ("cx", "min"):
+            lo = new("min", [va, vb])
+        if op in ("cx", "max"):
+            hi = new("max", [va, vb])
+        if op in ("cx", "min"):
+            cur[a] = lo
+        if op in ("cx", "max"):
+            cur[b] = hi
+    result = cur[out_slot]
+    # liveness: drop instructions not reaching the result
+    live = set()
+    stack = [result]
+    while stack:
+        v = stack.pop()
+        if v in live or v not in instrs:
+            continue
+        live.add(v)
+        stack.extend(instrs[v][1])
+    order = [o for o in order if o in live]
+    # fuse: x = k(a, b) used once, by y = k(x, c)  ->  y = k3(a, b, c)
+    changed = True
+    while changed:
+        changed = False
+        uses = {}
+        for o in order:
+            for sname in instrs[o][1]:
+                uses[sname] = uses.get(sname, 0) + 1
+        for o in order:
+            kind, srcs = instrs[o]
+            if len(srcs) != 2:
+                continue
+            for i, sname in enumerate(srcs):
+                if sname in instrs and uses.get(sname, 0) == 1 and sname != result:
+                    k2, s2 = instrs[sname]
+                    if k2 == kind and len(s2) == 2:
+                        instrs[o] = [kind, s2 + [srcs[1 - i]]]
+                        order.remove(sname)
+                        del instrs[sname]
+                        changed = True
+                        break
+            if changed:
+                break
+    return [(o, instrs[o][0], instrs[o][1]) for o in order], result
+
+
+def eval_ssa(instrs, result, values):
+    env = {f"x{i}": v for i, v in enumerate(values)}
+    for name, kind, srcs in instrs:
+        vals = [env[s] for s in srcs]
+        env[name] = min(vals) if kind == "min" else max(vals)
+    return env[result]
+
+
+def emit(n, ops, out_slot) -> str:
+    instrs, result = to_ssa(n, ops, out_slot)
+    rng = random.Random(7)
+    for _ in range(3000):
+        vals = [rng.randrange(0, rng.choice([2, 3, 16, 65536])) for _ in range(n)]
+        assert eval_ssa(instrs, result, vals) == sorted(vals)[(n - 1) // 2]
+    n3 = sum(1 for _, _, s in instrs if len(s) == 3)
+    lines = [f"// median of {n} values: {len(ops)} comparators -> {len(instrs)} packed u16x2 "
+             f"min/max instructions ({n3} of them 3-input)",
+             f"__device__ __forceinline__ uint32_t median_net_{n}(const uint32_t (&x)[{n}]) {{"]
+    for i in range(n):
+        lines.append(f"  const uint32_t x{i} = x[{i}];")
+    for name, kind, srcs in instrs:
+        fn = ("vmin" if kind == "min" else "vmax") + str(len(srcs))
+        lines.append(f"  const uint32_t {name} = {fn}({', '.join(srcs)});")
+    lines.append(f"  return {result};")
     lines.append("}")
     return "\n".join(lines)
 
@@ -160,12 +238,20 @@ def main():
            "}",
            "__device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) {",
            "  uint32_t r; asm(\"max.u16x2 %0, %1, %2;\" : \"=r\"(r) : \"r\"(a), \"r\"(b)); return r;",
+           "}",
+           "// 3-input forms: ptxas emits one VIMNMX3.U16x2 for each",
+           "__device__ __forceinline__ uint32_t vmin3(uint32_t a, uint32_t b, uint32_t c) {",
+           "  uint32_t r; asm(\"{.reg .b32 t; min.u16x2 t, %1, %2; min.u16x2 %0, t, %3;}\" : \"=r\"(r) : \"r\"(a), \"r\"(b), \"r\"(c)); return r;",
+           "}",
+           "__device__ __forceinline__ uint32_t vmax3(uint32_t a, uint32_t b, uint32_t c) {",
+           "  uint32_t r; asm(\"{.reg .b32 t; max.u16x2 t, %1, %2; max.u16x2 %0, t, %3;}\" : \"=r\"(r) : \"r\"(a), \"r\"(b), \"r\"(c)); return r;",
            "}", ""]
     for n in sizes:
         cost, ops, slot = build(n, (n - 1) // 2)
         check(n, ops, slot)
-        sys.stderr.write(f"n={n}: {len(ops)} comparators, {cost} ops\n")
-        out.append(emit(n, ops, slot))
+        text = emit(n, ops, slot)
+        sys.stderr.write(f"n={n}: {len(ops)} comparators, {cost} ops -> {text.splitlines()[0]}\n")
+        out.append(text)
         out.append("")
     out.append("}  // namespace irdn")
     print("\n".join(out))
