@@ -58,8 +58,8 @@ struct Geo {
   static constexpr int IN_STRIDE = (IN_BYTES + 127) & ~127;
   static constexpr int Q_OFF = NSTAGE * IN_STRIDE;
   static constexpr int BAR_OFF = Q_OFF + WARPS * STRIP_PX * 2;
-  static constexpr int TILE_OFF = BAR_OFF + 8 * NSTAGE;  // tile id staged in each buffer
-  static constexpr int SMEM = TILE_OFF + 4 * NSTAGE + 128;  // +128: runtime base alignment
+  static constexpr int TILE_OFF = BAR_OFF + 8 * NSTAGE;  // TileInfo staged with each buffer
+  static constexpr int SMEM = TILE_OFF + 16 * NSTAGE + 128;  // +128: runtime base alignment
   static_assert(BOXW <= 256 && BOXH <= 256, "TMA box limit");
 };
 
@@ -171,32 +171,52 @@ __device__ __forceinline__ uint32_t reduce_max(const uint32_t (&a)[N]) {
 }
 
 // Replicate-edge fix-up of the smem cells of a box that fall outside the frame.
+// Common case (frame wider than the box's halo on that side): the margin is exactly
+// ALIGN elements = 16 bytes per row, written with one 16-byte store per row.
 template <typename T, int K>
 __device__ __forceinline__ void fix_edges(T* s_in, int gx_lo, int gy_lo, int width, int height) {
   using G = Geo<T, K>;
-  constexpr int BOXW = G::BOXW, BOXH = G::BOXH;
+  constexpr int BOXW = G::BOXW, BOXH = G::BOXH, A = G::ALIGN;
   const int tid = threadIdx.x;
   const int c_lo = max(0, -gx_lo), c_hi = min(BOXW, width - gx_lo);   // in-frame columns
   const int y_lo = max(0, -gy_lo), y_hi = min(BOXH, height - gy_lo);  // in-frame rows
   const int ncl = c_lo, ncr = BOXW - c_hi;
-  const int nc = ncl + ncr;
   const int lane = tid & 31, warp = tid >> 5;
-  if (nc) {  // (a) left / right margins of in-frame rows: warps over rows, lanes over columns
-    for (int row = y_lo + warp; row < y_hi; row += WARPS) {
-      T* rp = s_in + row * BOXW;
-      for (int j = lane; j < nc; j += 32) {
-        const int col = j < ncl ? j : c_hi + (j - ncl);
-        rp[col] = rp[j < ncl ? c_lo : c_hi - 1];
+  if (ncl | ncr) {
+    if ((ncl == 0 || ncl == A) && (ncr == 0 || ncr == A)) {
+      // (a) one thread per (row, side): replicate the edge pixel over a 16-byte margin
+      for (int i = tid; i < 2 * (y_hi - y_lo); i += THREADS) {
+        const int row = y_lo + (i >> 1);
+        const bool left = (i & 1) == 0;
+        if (left ? ncl == 0 : ncr == 0) continue;
+        T* rp = s_in + row * BOXW;
+        uint32_t v = (uint32_t)rp[left ? c_lo : c_hi - 1];
+        if constexpr (sizeof(T) == 1) v *= 0x01010101u;
+        else v *= 0x00010001u;
+        const uint4 q = make_uint4(v, v, v, v);
+        *reinterpret_cast<uint4*>(rp + (left ? 0 : BOXW - A)) = q;
+      }
+    } else {
+      // (a') general margins: warps over rows, lanes over columns
+      const int nc = ncl + ncr;
+      for (int row = y_lo + warp; row < y_hi; row += WARPS) {
+        T* rp = s_in + row * BOXW;
+        for (int j = lane; j < nc; j += 32) {
+          const int col = j < ncl ? j : c_hi + (j - ncl);
+          rp[col] = rp[j < ncl ? c_lo : c_hi - 1];
+        }
       }
     }
     __syncthreads();
   }
+  // (b) rows above / below the frame copy the nearest in-frame row (corners included), 16 B at a time
   const int nrt = y_lo, nrb = BOXH - y_hi;
-  // (b) rows above / below the frame copy the nearest in-frame row (corners included)
-  for (int j = warp; j < nrt + nrb; j += WARPS) {
-    T* rp = s_in + (j < nrt ? j : y_hi + (j - nrt)) * BOXW;
-    const T* src = s_in + (j < nrt ? y_lo : y_hi - 1) * BOXW;
-    for (int col = lane; col < BOXW; col += 32) rp[col] = src[col];
+  constexpr int V = BOXW / A;  // 16-byte vectors per row
+  for (int i = tid; i < (nrt + nrb) * V; i += THREADS) {
+    const int j = i / V, col = (i - j * V) * A;
+    const int row = j < nrt ? j : y_hi + (j - nrt);
+    *reinterpret_cast<uint4*>(s_in + row * BOXW + col) =
+        *reinterpret_cast<const uint4*>(s_in + (j < nrt ? y_lo : y_hi - 1) * BOXW + col);
   }
 }
 
@@ -231,7 +251,50 @@ __device__ __forceinline__ uint32_t median_queue(const T* s_in, const uint16_t* 
   return replaced;
 }
 
+// Detector over one warp strip (see the file comment). FULL: the strip lies entirely
+// inside the frame, so no per-row / per-column validity checks are needed.
+template <typename T, int K, bool FULL>
+__device__ __forceinline__ void detect_strip(const T* s_in, int band0, int c0, T* outp, int64_t pitch, int valid_rows,
+                                             bool ok0, bool ok1, uint32_t (&flags)[2]) {
+  using G = Geo<T, K>;
+  constexpr int r = G::r, BOXW = G::BOXW;
+  constexpr int J = (r + 1) / 2;
+  uint32_t rmin[K], rmax[K], rcen[r + 1];
+  flags[0] = flags[1] = 0u;
+  const T* rowp = s_in + band0 * BOXW + c0;
+#pragma unroll
+  for (int s = 0; s < BAND + 2 * r; ++s) {
+    uint32_t wd[2 * J + 1];
+#pragma unroll
+    for (int j = -J; j <= J; ++j) wd[j + J] = load_pair<T>(rowp + s * BOXW, 2 * j);
+    uint32_t ops[K];  // lane-aligned operands for horizontal offsets -r..r
+#pragma unroll
+    for (int d = -r; d <= r; ++d)
+      ops[d + r] = (d & 1) == 0 ? wd[J + d / 2] : prmt(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], 0x5432u);
+    rmin[s % K] = reduce_min<K>(ops);
+    rmax[s % K] = reduce_max<K>(ops);
+    rcen[s % (r + 1)] = wd[J];
+    if (s >= 2 * r) {
+      const int y = s - 2 * r;  // output row within the strip
+      const uint32_t vmn = reduce_min<K>(rmin), vmx = reduce_max<K>(rmax);
+      const uint32_t c = rcen[(s - r) % (r + 1)];
+      // lane of m == 0  <=>  centre equals the window min or max (no borrow: vmn <= c <= vmx)
+      const uint32_t m = vmin2(c - vmn, vmx - c);
+      // m < 0x8000 per lane (it is at most (max-min)/2), so +0x7FFF sets bit 15 iff m != 0
+      const uint32_t e = m + 0x7FFF7FFFu;
+      flags[y >> 4] |= (~e & 0x80008000u) >> (15 - (y & 15));
+      if (FULL) store_pair_g<T>(outp, c, true, true);
+      else if (y < valid_rows) store_pair_g<T>(outp, c, ok0, ok1);
+      outp += pitch;
+    }
+  }
+}
+
 // ---- the kernel ----------------------------------------------------------------
+struct TileInfo {
+  int t, b, tx0, ty0;
+};
+
 template <typename T, int K>
 __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant__ CUtensorMap in_map,
                                                            const TileParams p) {
@@ -241,6 +304,7 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
   // TMA needs 128-byte aligned shared-memory boxes: align the dynamic base explicitly.
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + G::BAR_OFF);  // [NSTAGE] stage-full barriers
+  TileInfo* s_tile = reinterpret_cast<TileInfo*>(smem + G::TILE_OFF);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -249,26 +313,23 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
   const int ntiles = tiles_per_frame * p.batch;
   uint32_t replaced = 0, detected = 0;
 
-  auto tile_origin = [&](int t, int& b, int& tx0, int& ty0) {
-    b = t / tiles_per_frame;
-    const int tt = t - b * tiles_per_frame;
-    const int ty = tt / p.tiles_x;
-    tx0 = (tt - ty * p.tiles_x) * TW;
-    ty0 = p.row_begin + ty * TH;
-  };
-  int* s_tile = reinterpret_cast<int*>(smem + G::TILE_OFF);
-  // Dynamic tile scheduler (thread 0): grab the next tile, publish its id next to the
-  // stage, then arrive on the stage barrier (with the TMA bytes, or empty past the end).
-  // The barrier's release/acquire makes the id visible to every waiting thread.
+  // Dynamic tile scheduler (thread 0): grab the next tile, publish it next to the stage,
+  // then arrive on the stage barrier (with the TMA bytes, or empty past the end). The
+  // barrier's release/acquire makes the TileInfo visible to every waiting thread.
   auto refill = [&](int stage) {
-    const int t = (int)atomicAdd(p.sched, 1u);
-    s_tile[stage] = t;
-    if (t < ntiles) {
-      int b, tx0, ty0;
-      tile_origin(t, b, tx0, ty0);
+    TileInfo ti;
+    ti.t = (int)atomicAdd(p.sched, 1u);
+    if (ti.t < ntiles) {
+      ti.b = ti.t / tiles_per_frame;
+      const int tt = ti.t - ti.b * tiles_per_frame;
+      const int ty = tt / p.tiles_x;
+      ti.tx0 = (tt - ty * p.tiles_x) * TW;
+      ti.ty0 = p.row_begin + ty * TH;
+      s_tile[stage] = ti;
       mbar_expect_tx(&s_bar[stage], G::IN_BYTES);
-      tma_load_3d(smem + stage * G::IN_STRIDE, &in_map, &s_bar[stage], tx0 - R, ty0 - r - p.in_row0, b);
+      tma_load_3d(smem + stage * G::IN_STRIDE, &in_map, &s_bar[stage], ti.tx0 - R, ti.ty0 - r - p.in_row0, ti.b);
     } else {
+      s_tile[stage] = ti;
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_bar[stage])) : "memory");
     }
   };
@@ -291,62 +352,38 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
     const int stage = NSTAGE == 1 ? 0 : (iter % NSTAGE);
     T* s_in = reinterpret_cast<T*>(smem + stage * G::IN_STRIDE);
     mbar_wait(&s_bar[stage], (iter / NSTAGE) & 1);
-    const int t = s_tile[stage];
-    if (t >= ntiles) break;
-    int b, tx0, ty0;
-    tile_origin(t, b, tx0, ty0);
-    const int gx_lo = tx0 - R, gy_lo = ty0 - r;  // global coords of smem (0, 0)
+    const TileInfo ti = s_tile[stage];
+    if (ti.t >= ntiles) break;
+    const int gx_lo = ti.tx0 - R, gy_lo = ti.ty0 - r;  // global coords of smem (0, 0)
     if (gx_lo < 0 || gy_lo < 0 || gx_lo + BOXW > p.width || gy_lo + G::BOXH > p.height) {
       fix_edges<T, K>(s_in, gx_lo, gy_lo, p.width, p.height);
       __syncthreads();
     }
 
-    const int valid_w = min(TW, p.width - tx0);    // valid output columns in this tile
-    const int valid_h = min(TH, p.row_end - ty0);  // valid output rows
-    T* const out_tile = out_base + (int64_t)b * p.out_frame + (int64_t)(ty0 - p.row_begin) * p.out_pitch + tx0;
+    const int valid_w = min(TW, p.width - ti.tx0);    // valid output columns in this tile
+    const int valid_h = min(TH, p.row_end - ti.ty0);  // valid output rows
+    T* const out_tile =
+        out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.ty0 - p.row_begin) * p.out_pitch + ti.tx0;
     const bool ok0 = 2 * cpair < valid_w, ok1 = 2 * cpair + 1 < valid_w;
 
     if (p.method == 0) {
-      // ---- detector: horizontal K-wide min/max per input row, vertical K-row ring ----
-      constexpr int J = (r + 1) / 2;
-      uint32_t rmin[K], rmax[K], rcen[r + 1];
-      uint32_t flags[2] = {0u, 0u};
+      uint32_t flags[2];
+      T* outp = out_tile + (int64_t)band0 * p.out_pitch + 2 * cpair;
+      const int vr = min(BAND, max(0, valid_h - band0));
+      if (valid_w == TW && valid_h == TH) {
+        detect_strip<T, K, true>(s_in, band0, c0, outp, p.out_pitch, BAND, true, true, flags);
+      } else {
+        detect_strip<T, K, false>(s_in, band0, c0, outp, p.out_pitch, vr, ok0, ok1, flags);
+        // mask out pixels beyond the frame / strip
+        const uint32_t colm = (ok0 ? 0xFFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
 #pragma unroll
-      for (int s = 0; s < BAND + 2 * r; ++s) {
-        const T* row = s_in + (band0 + s) * BOXW;
-        uint32_t wd[2 * J + 1];
-#pragma unroll
-        for (int j = -J; j <= J; ++j) wd[j + J] = load_pair<T>(row, c0 + 2 * j);
-        uint32_t ops[K];  // lane-aligned operands for horizontal offsets -r..r
-#pragma unroll
-        for (int d = -r; d <= r; ++d)
-          ops[d + r] = (d & 1) == 0 ? wd[J + d / 2] : prmt(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], 0x5432u);
-        const uint32_t mn = reduce_min<K>(ops), mx = reduce_max<K>(ops);
-        rmin[s % K] = mn;
-        rmax[s % K] = mx;
-        rcen[s % (r + 1)] = wd[J];
-        if (s >= 2 * r) {
-          const int y = s - 2 * r;  // output row within the strip
-          const uint32_t vmn = reduce_min<K>(rmin), vmx = reduce_max<K>(rmax);
-          const uint32_t c = rcen[(s - r) % (r + 1)];
-          // lane of m == 0  <=>  centre equals the window min or max (no borrow: vmn <= c <= vmx)
-          const uint32_t m = vmin2(c - vmn, vmx - c);
-          // m < 0x8000 per lane (it is at most (max-min)/2), so +0x7FFF sets bit 15 iff m != 0
-          const uint32_t e = m + 0x7FFF7FFFu;
-          flags[y >> 4] |= (~e & 0x80008000u) >> (15 - (y & 15));
-          if (band0 + y < valid_h)
-            store_pair_g<T>(out_tile + (int64_t)(band0 + y) * p.out_pitch + 2 * cpair, c, ok0, ok1);
+        for (int h = 0; h < 2; ++h) {
+          const int v = min(16, max(0, vr - 16 * h));
+          const uint32_t rowm = v >= 16 ? 0xFFFFu : ((1u << v) - 1u);
+          flags[h] &= colm & (rowm | (rowm << 16));
         }
       }
-      // mask out pixels beyond the frame / strip, compact into the warp queue, median
-      const uint32_t colm = (ok0 ? 0xFFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
-      const int vr = min(BAND, max(0, valid_h - band0));
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int v = min(16, max(0, vr - 16 * h));
-        const uint32_t rowm = v >= 16 ? 0xFFFFu : ((1u << v) - 1u);
-        flags[h] &= colm & (rowm | (rowm << 16));
-      }
+      // compact the strip's noisy pixels into the warp queue
       const int cnt = __popc(flags[0]) + __popc(flags[1]);
       int incl = cnt;
 #pragma unroll
@@ -356,15 +393,16 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
       }
       const int n = __shfl_sync(0xffffffffu, incl, 31);
       detected += (uint32_t)cnt;
-      int pos = incl - cnt;
+      uint16_t* qp = s_q + (incl - cnt);
+      const uint32_t ebase = ((uint32_t)band0 << 8) | (uint32_t)(2 * cpair);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         uint32_t f = flags[h];
         while (f) {
           const int bit = __ffs(f) - 1;
           f &= f - 1u;
-          const int y = band0 + 16 * h + (bit & 15);
-          s_q[pos++] = (uint16_t)((y << 8) | (2 * cpair + (bit >> 4)));
+          // bit = lane*16 + row: entry = ((band0 + 16h + row) << 8) | (2*cpair + lane)
+          *qp++ = (uint16_t)(ebase + ((uint32_t)(16 * h + (bit & 15)) << 8) + (uint32_t)(bit >> 4));
         }
       }
       __syncwarp();  // queue visible; centre stores ordered before the median stores
