@@ -10,6 +10,7 @@
 #include <string>
 #include "fnr_common.cuh"
 #include "fnr_tile.cuh"
+#include "fnr_k3.cuh"
 
 namespace irdn {
 void note_launch();
@@ -146,6 +147,62 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   return 0;
 }
 
+// Dense 3x3 kernel for u8 frames (fnr_k3.cuh).
+inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int method,
+                     unsigned long long* counts, cudaStream_t s, bool* taken) {
+  using G = k3::Geo;
+  *taken = false;
+  CUtensorMap in_map;
+  const int out_rows = g.row_end - g.row_begin;
+  if (!make_map<uint8_t>(&in_map, d_in, g.width, g.in_rows, g.batch, g.in_pitch, g.in_frame_stride, G::BOXW,
+                         G::BOXH))
+    return 0;
+  const bool full_w = g.width % k3::TW == 0;
+  static int bps[2] = {0, 0};
+  int& blocks_per_sm = bps[full_w ? 1 : 0];
+  auto kern = full_w ? k3::fnr_k3_kernel<true> : k3::fnr_k3_kernel<false>;
+  if (blocks_per_sm == 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, k3::THREADS, G::SMEM) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = 1;
+    }
+    blocks_per_sm = n;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  unsigned int* sched = sched_slot(dev);
+  if (!sched) return 0;
+  tile::TileParams p;
+  p.out = d_out;
+  p.out_pitch = g.out_pitch;
+  p.out_frame = g.out_frame_stride;
+  p.width = g.width;
+  p.height = g.height;
+  p.in_row0 = g.in_row0;
+  p.row_begin = g.row_begin;
+  p.row_end = g.row_end;
+  p.tiles_x = (g.width + k3::TW - 1) / k3::TW;
+  p.tiles_y = (out_rows + k3::TH - 1) / k3::TH;
+  p.batch = g.batch;
+  p.method = method;
+  p.counts = counts;
+  p.sched = sched;
+  const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
+  if (ntiles > 0x7fffffffLL) return 0;
+  dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));
+  *taken = true;
+  kern<<<grid, k3::THREADS, G::SMEM, s>>>(in_map, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_fast_err = cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
+
 template <typename T>
 inline bool try_launch(const T* d_in, T* d_out, const PassGeom& g, int k, int method, unsigned long long* counts,
                        cudaStream_t s, int* rc) {
@@ -157,7 +214,10 @@ inline bool try_launch(const T* d_in, T* d_out, const PassGeom& g, int k, int me
   bool taken = false;
   int e = 0;
   switch (k) {
-    case 3: e = launch_tile<T, 3>(d_in, d_out, g, method, counts, s, &taken); break;
+    case 3:
+      if constexpr (sizeof(T) == 1) e = launch_k3(d_in, d_out, g, method, counts, s, &taken);
+      else e = launch_tile<T, 3>(d_in, d_out, g, method, counts, s, &taken);
+      break;
     case 5: e = launch_tile<T, 5>(d_in, d_out, g, method, counts, s, &taken); break;
     case 7: e = launch_tile<T, 7>(d_in, d_out, g, method, counts, s, &taken); break;
     case 9: e = launch_tile<T, 9>(d_in, d_out, g, method, counts, s, &taken); break;
