@@ -134,6 +134,7 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.method = method;
   p.counts = counts;
   p.sched = sched;
+  p.one = 1u;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));
@@ -190,6 +191,7 @@ inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int
   p.method = method;
   p.counts = counts;
   p.sched = sched;
+  p.one = 1u;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));

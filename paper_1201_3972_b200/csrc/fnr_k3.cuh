@@ -48,8 +48,31 @@ struct Geo {
   static constexpr int SMEM = TILE_OFF + 16 * NSTAGE + 128;
 };
 
-__device__ __forceinline__ uint32_t med3(uint32_t a, uint32_t b, uint32_t c) {
-  return a + b + c - vmin3(a, b, c) - vmax3(a, b, c);  // exact: the true median fits each lane
+// Integer multiply-add on the FMA pipe. `one` is an opaque runtime 1 (a kernel argument), so
+// ptxas keeps IMAD instead of turning the add into IADD3, which would compete with the
+// VIMNMX3 / PRMT / LOP3 stream for the ALU pipe (measured ALU-bound at 92%).
+__device__ __forceinline__ uint32_t fma_add(uint32_t a, uint32_t one, uint32_t b) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+  return r;
+}
+// a - b on the FMA pipe (b * 0xFFFFFFFF + a).
+__device__ __forceinline__ uint32_t fma_sub(uint32_t a, uint32_t minus_one, uint32_t b) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(minus_one), "r"(a));
+  return r;
+}
+// (a >> 16) | (b << 16) with two IMADs instead of one PRMT (moves the shift to the FMA pipe).
+__device__ __forceinline__ uint32_t shift_pair(uint32_t a, uint32_t b, uint32_t k65536) {
+  uint32_t hi, r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(a), "r"(k65536));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(k65536), "r"(hi));
+  return r;
+}
+// Median of three packed keys: a + b + c - min - max (exact in 32-bit: the true median
+// fits each lane). The 3-input sum stays one IADD3; the subtraction goes to the FMA pipe.
+__device__ __forceinline__ uint32_t med3(uint32_t a, uint32_t b, uint32_t c, uint32_t m1) {
+  return fma_sub(fma_sub(a + b + c, m1, vmin3(a, b, c)), m1, vmax3(a, b, c));
 }
 
 // Replicate-edge fix-up (see tile::fix_edges) for this kernel's box.
@@ -123,6 +146,7 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
   const int tiles_per_frame = p.tiles_x * p.tiles_y;
   const int ntiles = tiles_per_frame * p.batch;
   const bool fnr = p.method == 0;
+  const uint32_t one = p.one, m1 = 0u - p.one, k65536 = p.one << 16;  // opaque constants for the FMA pipe
   uint32_t det_total = 0, rep_total = 0;
 
   auto refill = [&](int stage) {
@@ -189,10 +213,10 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
       uint32_t lo[COLS + 2], hi[COLS + 2], mid[COLS + 2], S[COLS + 2];
 #pragma unroll
       for (int c = 0; c < COLS + 2; ++c) {
-        S[c] = tile::prmt(A[c], B[c], 0x5432u);  // rows y, y+1
+        S[c] = shift_pair(A[c], B[c], k65536);  // rows y, y+1
         lo[c] = vmin3(A[c], S[c], B[c]);
         hi[c] = vmax3(A[c], S[c], B[c]);
-        mid[c] = A[c] + S[c] + B[c] - lo[c] - hi[c];
+        mid[c] = fma_sub(fma_sub(A[c] + S[c] + B[c], m1, lo[c]), m1, hi[c]);
         A[c] = B[c];
       }
       const int yr = y0 + 2 * s;  // tile row of lane 0
@@ -200,18 +224,18 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
       uint32_t out[COLS];
 #pragma unroll
       for (int i = 0; i < COLS; ++i) {
-        const uint32_t med = med3(vmax3(lo[i], lo[i + 1], lo[i + 2]), med3(mid[i], mid[i + 1], mid[i + 2]),
-                                  vmin3(hi[i], hi[i + 1], hi[i + 2]));
+        const uint32_t med = med3(vmax3(lo[i], lo[i + 1], lo[i + 2]), med3(mid[i], mid[i + 1], mid[i + 2], m1),
+                                  vmin3(hi[i], hi[i + 1], hi[i + 2]), m1);
         if (fnr) {
           const uint32_t c = S[i + 1];
           const uint32_t mn = vmin3(lo[i], lo[i + 1], lo[i + 2]), mx = vmax3(hi[i], hi[i + 1], hi[i + 2]);
           // lane of m == 0 <=> centre is the window min or max; m <= 0x7FFF so +0x7FFF sets bit 15 iff m != 0
-          const uint32_t e = vmin2(c - mn, mx - c) + 0x7FFF7FFFu;
+          const uint32_t e = fma_add(vmin2(fma_sub(c, m1, mn), fma_sub(mx, m1, c)), one, 0x7FFF7FFFu);
           uint32_t keep = tile::prmt(e, e, 0xBB99u);  // 0xFFFF lanes: signal pixel, keep the centre
           keep |= rowkeep | colkeep[i];
           out[i] = (c & keep) | (med & ~keep);
-          keep_acc += keep;                                     // decoded per tile (see below)
-          rep_acc += vmin2((med ^ c) & ~keep, 0x00010001u);     // noisy and changed
+          keep_acc = fma_add(keep, one, keep_acc);                          // decoded per tile (see below)
+          rep_acc = fma_add(vmin2((med ^ c) & ~keep, 0x00010001u), one, rep_acc);  // noisy and changed
         } else {
           out[i] = med;
         }

@@ -78,6 +78,7 @@ struct TileParams {
   int32_t method;     // 0 fnr, 1 mf
   unsigned long long* counts;
   unsigned int* sched;  // [0] next tile to hand out, [1] finished CTAs (reset to 0 by the last CTA)
+  uint32_t one;         // 1, opaque to the compiler (keeps adds as IMAD on the FMA pipe)
 };
 
 // ---- PTX helpers ------------------------------------------------------------

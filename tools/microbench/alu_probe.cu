@@ -44,6 +44,10 @@ __global__ void alu_kernel(uint32_t* out, uint32_t seed) {
       if (OP == 10) { uint32_t t; if (i & 1) asm volatile("min.f16x2 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); else asm volatile("min.u16x2 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // mixed
       if (OP == 11) { uint32_t t; asm volatile("min.f32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // FMNMX
       if (OP == 12) { uint32_t t; if (i & 1) asm volatile("add.u32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); else asm volatile("min.u16x2 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // VIMNMX + IADD mix
+      if (OP == 13) { uint32_t t; asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(v[i]), "r"(c), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // IMAD reg
+      if (OP == 14) { uint32_t t; asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(c)); v[i] = t ^ b; }  // IMAD.HI (+LOP3)
+      if (OP == 15) { uint32_t t; if (i & 1) asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(v[i]), "r"(c), "r"(v[(i + 1) % CHAINS])); else asm volatile("{.reg .b32 q; min.u16x2 q, %1, %2; min.u16x2 %0, q, %3;}" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS]), "r"(b)); v[i] = t; }  // VIMNMX3 + IMAD
+      if (OP == 16) { uint32_t t; asm volatile("add.u32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); asm volatile("add.u32 %0, %0, %1;" : "+r"(t) : "r"(b)); v[i] = t; }  // IADD3
       if (OP == 7) { uint32_t t; asm volatile("min.u32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // IMNMX.U32
     }
   }
@@ -101,6 +105,10 @@ int main() {
   run_alu<10>("mixed_vimnmx_hmnmx2", 1);
   run_alu<11>("fmnmx_f32", 1);
   run_alu<12>("mixed_vimnmx_iadd", 1);
+  run_alu<13>("imad_reg", 1);
+  run_alu<14>("imad_hi_plus_lop3", 2);
+  run_alu<15>("mixed_vimnmx3_imad", 1);
+  run_alu<16>("iadd3_3input", 1);
 
   // HBM copy: 2 GiB in + 2 GiB out
   size_t bytes = (size_t)2 << 30;
