@@ -25,6 +25,32 @@ struct PassGeom {
   int32_t batch;
 };
 
+// ---- FMA-pipe integer helpers -------------------------------------------------
+// On sm_100a VIMNMX(3), PRMT, LOP3, SHF and IADD3 all issue on the ALU pipe (64
+// lanes/clk/SM, measured: profiles/alu_probe_r01.txt) while IMAD issues on the FMA
+// pipe at the same rate. The min/max-heavy kernels are ALU-bound, so adds, subtracts
+// and shifts that are not min/max go to the FMA pipe as IMADs.
+// Integer multiply-add on the FMA pipe. `one` is an opaque runtime 1 (a kernel argument), so
+// ptxas keeps IMAD instead of turning the add into IADD3, which would compete with the
+// VIMNMX3 / PRMT / LOP3 stream for the ALU pipe (measured ALU-bound at 92%).
+__device__ __forceinline__ uint32_t fma_add(uint32_t a, uint32_t one, uint32_t b) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+  return r;
+}
+// a - b on the FMA pipe (b * 0xFFFFFFFF + a).
+__device__ __forceinline__ uint32_t fma_sub(uint32_t a, uint32_t minus_one, uint32_t b) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(minus_one), "r"(a));
+  return r;
+}
+// (a >> 16) | (b << 16) with two IMADs instead of one PRMT (moves the shift to the FMA pipe).
+__device__ __forceinline__ uint32_t shift_pair(uint32_t a, uint32_t b, uint32_t k65536) {
+  uint32_t hi, r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(a), "r"(k65536));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(k65536), "r"(hi));
+  return r;
+}
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // Block-wide reduction of the two FNR counters followed by ONE 64-bit atomic

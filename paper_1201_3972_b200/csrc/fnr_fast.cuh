@@ -6,6 +6,7 @@
 // else goes to the generic kernel (fnr_generic.cuh) — still sm_100a code.
 #pragma once
 #include <cuda.h>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include "fnr_common.cuh"
@@ -135,6 +136,7 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.counts = counts;
   p.sched = sched;
   p.one = 1u;
+  p.debug = getenv("IRDN_DEBUG") ? atoi(getenv("IRDN_DEBUG")) : 0;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));

@@ -48,27 +48,6 @@ struct Geo {
   static constexpr int SMEM = TILE_OFF + 16 * NSTAGE + 128;
 };
 
-// Integer multiply-add on the FMA pipe. `one` is an opaque runtime 1 (a kernel argument), so
-// ptxas keeps IMAD instead of turning the add into IADD3, which would compete with the
-// VIMNMX3 / PRMT / LOP3 stream for the ALU pipe (measured ALU-bound at 92%).
-__device__ __forceinline__ uint32_t fma_add(uint32_t a, uint32_t one, uint32_t b) {
-  uint32_t r;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
-  return r;
-}
-// a - b on the FMA pipe (b * 0xFFFFFFFF + a).
-__device__ __forceinline__ uint32_t fma_sub(uint32_t a, uint32_t minus_one, uint32_t b) {
-  uint32_t r;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(minus_one), "r"(a));
-  return r;
-}
-// (a >> 16) | (b << 16) with two IMADs instead of one PRMT (moves the shift to the FMA pipe).
-__device__ __forceinline__ uint32_t shift_pair(uint32_t a, uint32_t b, uint32_t k65536) {
-  uint32_t hi, r;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(a), "r"(k65536));
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(k65536), "r"(hi));
-  return r;
-}
 // Median of three packed keys: a + b + c - min - max (exact in 32-bit: the true median
 // fits each lane). The 3-input sum stays one IADD3; the subtraction goes to the FMA pipe.
 __device__ __forceinline__ uint32_t med3(uint32_t a, uint32_t b, uint32_t c, uint32_t m1) {

@@ -26,7 +26,7 @@
 #include "select_nets.cuh"
 
 #ifndef IRDN_NSTAGE
-#define IRDN_NSTAGE 1
+#define IRDN_NSTAGE 2
 #endif
 
 namespace irdn {
@@ -35,11 +35,15 @@ namespace tile {
 constexpr int THREADS = 128;
 constexpr int WARPS = THREADS / 32;
 constexpr int TW = 128;                 // output tile width (pixels) = 2 warps x 32 pixel pairs
-constexpr int TH = 64;                  // output tile height (rows)
-constexpr int BAND = TH / (WARPS / 2);  // rows walked by one thread (two 16-row flag words)
+#ifndef IRDN_TH
+#define IRDN_TH 32
+#endif
+constexpr int TH = IRDN_TH;             // output tile height (rows)
+constexpr int BAND = TH / (WARPS / 2);  // rows walked by one thread
+constexpr int NFW = BAND / 16;          // 16-row flag words per thread
 constexpr int STRIP_PX = 64 * BAND;     // pixels of one warp strip (queue capacity)
 constexpr int NSTAGE = IRDN_NSTAGE;     // input stages (2 = double-buffered TMA)
-static_assert(BAND == 32, "two 16-row flag words per thread");
+static_assert(BAND % 16 == 0 && NFW >= 1, "whole 16-row flag words per thread");
 
 template <typename T, int K>
 struct Geo {
@@ -79,6 +83,7 @@ struct TileParams {
   unsigned long long* counts;
   unsigned int* sched;  // [0] next tile to hand out, [1] finished CTAs (reset to 0 by the last CTA)
   uint32_t one;         // 1, opaque to the compiler (keeps adds as IMAD on the FMA pipe)
+  int32_t debug;        // experiments only: 1 = skip the median stage, 2 = skip the network
 };
 
 // ---- PTX helpers ------------------------------------------------------------
@@ -229,6 +234,8 @@ __device__ __forceinline__ uint32_t median_queue(const T* s_in, const uint16_t* 
   using G = Geo<T, K>;
   constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
   uint32_t replaced = 0;
+  const bool skip_net = n < 0;
+  if (skip_net) n = -n;
   for (int i = lane; 2 * i < n; i += 32) {
     const uint32_t e0 = q[2 * i];
     const bool two = 2 * i + 1 < n;
@@ -243,7 +250,7 @@ __device__ __forceinline__ uint32_t median_queue(const T* s_in, const uint16_t* 
 #pragma unroll
       for (int dx = 0; dx < K; ++dx)
         v[dy * K + dx] = (uint32_t)a[dy * BOXW + dx] | ((uint32_t)bb[dy * BOXW + dx] << 16);
-    const uint32_t med = median_dispatch<K * K>(v);
+    const uint32_t med = skip_net ? (v[0] ^ v[K * K - 1] ^ v[K * K / 2]) : median_dispatch<K * K>(v);
     const uint32_t m0 = med & 0xFFFFu, m1 = med >> 16;
     out_tile[y0 * pitch + x0] = (T)m0;
     if (two) out_tile[y1 * pitch + x1] = (T)m1;
@@ -256,12 +263,14 @@ __device__ __forceinline__ uint32_t median_queue(const T* s_in, const uint16_t* 
 // inside the frame, so no per-row / per-column validity checks are needed.
 template <typename T, int K, bool FULL>
 __device__ __forceinline__ void detect_strip(const T* s_in, int band0, int c0, T* outp, int64_t pitch, int valid_rows,
-                                             bool ok0, bool ok1, uint32_t (&flags)[2]) {
+                                             bool ok0, bool ok1, uint32_t (&flags)[NFW], uint32_t one) {
+  const uint32_t m1 = 0u - one, k65536 = one << 16, k2p31 = one << 31;
   using G = Geo<T, K>;
   constexpr int r = G::r, BOXW = G::BOXW;
   constexpr int J = (r + 1) / 2;
   uint32_t rmin[K], rmax[K], rcen[r + 1];
-  flags[0] = flags[1] = 0u;
+#pragma unroll
+  for (int h = 0; h < NFW; ++h) flags[h] = 0u;
   const T* rowp = s_in + band0 * BOXW + c0;
 #pragma unroll
   for (int s = 0; s < BAND + 2 * r; ++s) {
@@ -271,7 +280,7 @@ __device__ __forceinline__ void detect_strip(const T* s_in, int band0, int c0, T
     uint32_t ops[K];  // lane-aligned operands for horizontal offsets -r..r
 #pragma unroll
     for (int d = -r; d <= r; ++d)
-      ops[d + r] = (d & 1) == 0 ? wd[J + d / 2] : prmt(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], 0x5432u);
+      ops[d + r] = (d & 1) == 0 ? wd[J + d / 2] : shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536);
     rmin[s % K] = reduce_min<K>(ops);
     rmax[s % K] = reduce_max<K>(ops);
     rcen[s % (r + 1)] = wd[J];
@@ -280,10 +289,14 @@ __device__ __forceinline__ void detect_strip(const T* s_in, int band0, int c0, T
       const uint32_t vmn = reduce_min<K>(rmin), vmx = reduce_max<K>(rmax);
       const uint32_t c = rcen[(s - r) % (r + 1)];
       // lane of m == 0  <=>  centre equals the window min or max (no borrow: vmn <= c <= vmx)
-      const uint32_t m = vmin2(c - vmn, vmx - c);
+      const uint32_t m = vmin2(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c));
       // m < 0x8000 per lane (it is at most (max-min)/2), so +0x7FFF sets bit 15 iff m != 0
-      const uint32_t e = m + 0x7FFF7FFFu;
-      flags[y >> 4] |= (~e & 0x80008000u) >> (15 - (y & 15));
+      const uint32_t e = fma_add(m, one, 0x7FFF7FFFu);
+      // shift the row history down one bit (IMAD.HI on the FMA pipe) and insert this
+      // row's "noisy" bits at 15 / 31; after 16 rows row i sits at bits i and 16 + i
+      uint32_t sh;
+      asm("mul.hi.u32 %0, %1, %2;" : "=r"(sh) : "r"(flags[y >> 4]), "r"(k2p31));
+      flags[y >> 4] = (sh & 0x7FFF7FFFu) | (~e & 0x80008000u);
       if (FULL) store_pair_g<T>(outp, c, true, true);
       else if (y < valid_rows) store_pair_g<T>(outp, c, ok0, ok1);
       outp += pitch;
@@ -317,22 +330,43 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
   // Dynamic tile scheduler (thread 0): grab the next tile, publish it next to the stage,
   // then arrive on the stage barrier (with the TMA bytes, or empty past the end). The
   // barrier's release/acquire makes the TileInfo visible to every waiting thread.
-  auto refill = [&](int stage) {
+  auto origin = [&](int t) {
     TileInfo ti;
-    ti.t = (int)atomicAdd(p.sched, 1u);
-    if (ti.t < ntiles) {
-      ti.b = ti.t / tiles_per_frame;
-      const int tt = ti.t - ti.b * tiles_per_frame;
-      const int ty = tt / p.tiles_x;
-      ti.tx0 = (tt - ty * p.tiles_x) * TW;
-      ti.ty0 = p.row_begin + ty * TH;
+    ti.t = t;
+    ti.b = t / tiles_per_frame;
+    const int tt = t - ti.b * tiles_per_frame;
+    const int ty = tt / p.tiles_x;
+    ti.tx0 = (tt - ty * p.tiles_x) * TW;
+    ti.ty0 = p.row_begin + ty * TH;
+    return ti;
+  };
+  // Thread 0 keeps the id of the tile it will load next (`ahead`) and asks the TMA unit to
+  // pull that tile into L2 while the current one is filtered, so the smem load that
+  // follows the end-of-tile barrier is served from L2.
+  int ahead = 0;
+  auto grab_ahead = [&]() {
+    ahead = (int)atomicAdd(p.sched, 1u);
+    if (ahead < ntiles) {
+      const TileInfo ti = origin(ahead);
+      asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(&in_map),
+                   "r"(ti.tx0 - R), "r"(ti.ty0 - r - p.in_row0), "r"(ti.b)
+                   : "memory");
+    }
+  };
+  auto refill = [&](int stage) {
+    const int t = ahead;
+    TileInfo ti;
+    if (t < ntiles) {
+      ti = origin(t);
       s_tile[stage] = ti;
       mbar_expect_tx(&s_bar[stage], G::IN_BYTES);
       tma_load_3d(smem + stage * G::IN_STRIDE, &in_map, &s_bar[stage], ti.tx0 - R, ti.ty0 - r - p.in_row0, ti.b);
     } else {
+      ti.t = t;
       s_tile[stage] = ti;
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_bar[stage])) : "memory");
     }
+    grab_ahead();
   };
 
   if (tid == 0) {
@@ -340,6 +374,7 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
     for (int s = 0; s < NSTAGE; ++s) mbar_init(&s_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
+    grab_ahead();
     for (int s = 0; s < NSTAGE; ++s) refill(s);
   }
   __syncthreads();
@@ -368,24 +403,26 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
     const bool ok0 = 2 * cpair < valid_w, ok1 = 2 * cpair + 1 < valid_w;
 
     if (p.method == 0) {
-      uint32_t flags[2];
+      uint32_t flags[NFW];
       T* outp = out_tile + (int64_t)band0 * p.out_pitch + 2 * cpair;
       const int vr = min(BAND, max(0, valid_h - band0));
       if (valid_w == TW && valid_h == TH) {
-        detect_strip<T, K, true>(s_in, band0, c0, outp, p.out_pitch, BAND, true, true, flags);
+        detect_strip<T, K, true>(s_in, band0, c0, outp, p.out_pitch, BAND, true, true, flags, p.one);
       } else {
-        detect_strip<T, K, false>(s_in, band0, c0, outp, p.out_pitch, vr, ok0, ok1, flags);
+        detect_strip<T, K, false>(s_in, band0, c0, outp, p.out_pitch, vr, ok0, ok1, flags, p.one);
         // mask out pixels beyond the frame / strip
         const uint32_t colm = (ok0 ? 0xFFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < NFW; ++h) {
           const int v = min(16, max(0, vr - 16 * h));
           const uint32_t rowm = v >= 16 ? 0xFFFFu : ((1u << v) - 1u);
           flags[h] &= colm & (rowm | (rowm << 16));
         }
       }
       // compact the strip's noisy pixels into the warp queue
-      const int cnt = __popc(flags[0]) + __popc(flags[1]);
+      int cnt = 0;
+#pragma unroll
+      for (int h = 0; h < NFW; ++h) cnt += __popc(flags[h]);
       int incl = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -397,7 +434,7 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
       uint16_t* qp = s_q + (incl - cnt);
       const uint32_t ebase = ((uint32_t)band0 << 8) | (uint32_t)(2 * cpair);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < NFW; ++h) {
         uint32_t f = flags[h];
         while (f) {
           const int bit = __ffs(f) - 1;
@@ -407,7 +444,7 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
         }
       }
       __syncwarp();  // queue visible; centre stores ordered before the median stores
-      replaced += median_queue<T, K>(s_in, s_q, n, out_tile, p.out_pitch, lane, true);
+      if (p.debug != 1) replaced += median_queue<T, K>(s_in, s_q, p.debug == 2 ? -n : n, out_tile, p.out_pitch, lane, true);
       __syncwarp();
     } else {
       // MF: every valid pixel of the strip through the same queue
