@@ -12,6 +12,7 @@
 #include "fnr_common.cuh"
 #include "fnr_tile.cuh"
 #include "fnr_k3.cuh"
+#include "fnr_warp.cuh"
 
 namespace irdn {
 void note_launch();
@@ -150,6 +151,73 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   return 0;
 }
 
+// Warp-autonomous kernel (fnr_warp.cuh): 64 x 32 warp tiles, per-warp TMA ring.
+template <typename T, int K>
+inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, unsigned long long* counts,
+                       cudaStream_t s, bool* taken) {
+  using G = wk::Geo<T, K>;
+  *taken = false;
+  CUtensorMap in_map;
+  const int out_rows = g.row_end - g.row_begin;
+  if (!make_map<T>(&in_map, d_in, g.width, g.in_rows, g.batch, g.in_pitch, g.in_frame_stride, G::BOXW, G::BOXH))
+    return 0;
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    cudaFuncSetAttribute(wk::fnr_warp_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wk::fnr_warp_kernel<T, K>, wk::THREADS, G::SMEM) !=
+            cudaSuccess ||
+        n < 1) {
+      cudaGetLastError();
+      n = 1;
+    }
+    blocks_per_sm = n;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  unsigned int* sched = sched_slot(dev);
+  if (!sched) return 0;
+  tile::TileParams p;
+  p.out = d_out;
+  p.out_pitch = g.out_pitch;
+  p.out_frame = g.out_frame_stride;
+  p.width = g.width;
+  p.height = g.height;
+  p.in_row0 = g.in_row0;
+  p.row_begin = g.row_begin;
+  p.row_end = g.row_end;
+  p.tiles_x = (g.width + wk::WW - 1) / wk::WW;
+  p.tiles_y = (out_rows + wk::WH - 1) / wk::WH;
+  p.batch = g.batch;
+  p.method = method;
+  p.counts = counts;
+  p.sched = sched;
+  p.one = 1u;
+  p.debug = 0;
+  const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
+  if (ntiles > 0x7fffffffLL) return 0;
+  const long long ctas = std::max<long long>(1, std::min<long long>((ntiles + wk::WARPS - 1) / wk::WARPS,
+                                                                    (long long)sms * blocks_per_sm));
+  *taken = true;
+  wk::fnr_warp_kernel<T, K><<<(unsigned)ctas, wk::THREADS, G::SMEM, s>>>(in_map, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_fast_err = cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
+
+inline bool use_tile_kernel() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IRDN_KERNEL");
+    v = (e && e[0] == 't') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // Dense 3x3 kernel for u8 frames (fnr_k3.cuh).
 inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int method,
                      unsigned long long* counts, cudaStream_t s, bool* taken) {
@@ -217,15 +285,21 @@ inline bool try_launch(const T* d_in, T* d_out, const PassGeom& g, int k, int me
   if (g.width < 16 || g.height < 1) return false;
   bool taken = false;
   int e = 0;
+  const bool tile_k = use_tile_kernel();
   switch (k) {
     case 3:
       if constexpr (sizeof(T) == 1) e = launch_k3(d_in, d_out, g, method, counts, s, &taken);
-      else e = launch_tile<T, 3>(d_in, d_out, g, method, counts, s, &taken);
+      else e = tile_k ? launch_tile<T, 3>(d_in, d_out, g, method, counts, s, &taken)
+                      : launch_warp<T, 3>(d_in, d_out, g, method, counts, s, &taken);
       break;
-    case 5: e = launch_tile<T, 5>(d_in, d_out, g, method, counts, s, &taken); break;
-    case 7: e = launch_tile<T, 7>(d_in, d_out, g, method, counts, s, &taken); break;
-    case 9: e = launch_tile<T, 9>(d_in, d_out, g, method, counts, s, &taken); break;
-    case 11: e = launch_tile<T, 11>(d_in, d_out, g, method, counts, s, &taken); break;
+    case 5: e = tile_k ? launch_tile<T, 5>(d_in, d_out, g, method, counts, s, &taken)
+                       : launch_warp<T, 5>(d_in, d_out, g, method, counts, s, &taken); break;
+    case 7: e = tile_k ? launch_tile<T, 7>(d_in, d_out, g, method, counts, s, &taken)
+                       : launch_warp<T, 7>(d_in, d_out, g, method, counts, s, &taken); break;
+    case 9: e = tile_k ? launch_tile<T, 9>(d_in, d_out, g, method, counts, s, &taken)
+                       : launch_warp<T, 9>(d_in, d_out, g, method, counts, s, &taken); break;
+    case 11: e = tile_k ? launch_tile<T, 11>(d_in, d_out, g, method, counts, s, &taken)
+                        : launch_warp<T, 11>(d_in, d_out, g, method, counts, s, &taken); break;
     default: return false;
   }
   if (!taken) return false;

@@ -1,0 +1,283 @@
+// Warp-autonomous FNR / MF kernel (sm_100a): every warp streams its own 64 x 32 tiles.
+//
+// The flagged-pixel median work is irregular (2-50 % of pixels, clustered by scene
+// content), so CTA-wide tiles leave warps waiting at barriers for the slowest warp
+// and for the next tile's load. Here each warp is its own pipeline:
+//   * a dynamic scheduler hands out 64 x 32 warp tiles (one atomic per tile);
+//   * lane 0 stages the tile plus halo with TMA (cp.async.bulk.tensor.3d) into the
+//     warp's own shared-memory ring (NSTAGE deep, one mbarrier per stage), issuing
+//     the load of the warp's next tile as soon as a stage is released — so the load
+//     runs while the current tile is filtered, and no CTA barrier exists at all;
+//   * detector (filters.py:169-171) and median (filters.py:172-176) exactly as in
+//     fnr_tile.cuh: each lane owns one column pair (u16x2) walking the 32 rows, noisy
+//     pixels are compacted with one warp scan into the warp's queue, and each lane
+//     runs one median-selection network per two queued pixels.
+// Frame borders: TMA zero-fills out-of-frame cells; the warp overwrites them with the
+// nearest in-frame cell (replicate edge, image.py:117-130) before filtering.
+#pragma once
+#include "fnr_tile.cuh"
+
+namespace irdn {
+namespace wk {
+
+constexpr int WARPS = 2;               // warps per CTA (packaging only: no CTA barriers)
+constexpr int THREADS = 32 * WARPS;
+constexpr int WW = 64;                 // warp tile width: 32 lanes x 2 pixels
+constexpr int WH = 32;                 // warp tile height
+constexpr int NSTAGE = 2;
+constexpr int QCAP = WW * WH;          // queue entries (every pixel may be noisy)
+
+template <typename T, int K>
+struct Geo {
+  static constexpr int r = K / 2;
+  static constexpr int A = 16 / (int)sizeof(T);  // TMA x start: 16-byte aligned
+  static constexpr int R = A;
+  static_assert(r <= R, "window radius exceeds the aligned halo");
+  static constexpr int BOXW = ((WW + R + r + A - 1) / A) * A;
+  static constexpr int BOXH = WH + 2 * r;
+  static constexpr int IN_BYTES = BOXW * BOXH * (int)sizeof(T);
+  static constexpr int STAGE = (IN_BYTES + 127) & ~127;
+  static constexpr int Q_OFF = NSTAGE * STAGE;
+  static constexpr int BAR_OFF = Q_OFF + QCAP * 2;
+  static constexpr int INFO_OFF = BAR_OFF + 8 * NSTAGE;
+  static constexpr int WARP_BYTES = (INFO_OFF + 16 * NSTAGE + 127) & ~127;
+  static constexpr int SMEM = WARPS * WARP_BYTES + 128;
+};
+
+struct WTile {
+  int t, b, x0, y0;
+};
+
+// replicate-edge fix-up of one warp's box (cells outside the frame)
+template <typename T, int K>
+__device__ __forceinline__ void fix_edges_warp(T* s_in, int gx_lo, int gy_lo, int width, int height, int lane) {
+  using G = Geo<T, K>;
+  constexpr int BOXW = G::BOXW, BOXH = G::BOXH, A = G::A;
+  const int c_lo = max(0, -gx_lo), c_hi = min(BOXW, width - gx_lo);
+  const int y_lo = max(0, -gy_lo), y_hi = min(BOXH, height - gy_lo);
+  const int ncl = c_lo, ncr = BOXW - c_hi;
+  if (ncl | ncr) {
+    if ((ncl == 0 || ncl == A) && (ncr == 0 || ncr == A)) {
+      for (int i = lane; i < 2 * (y_hi - y_lo); i += 32) {
+        const int row = y_lo + (i >> 1);
+        const bool left = (i & 1) == 0;
+        if (left ? ncl == 0 : ncr == 0) continue;
+        T* rp = s_in + row * BOXW;
+        uint32_t v = (uint32_t)rp[left ? c_lo : c_hi - 1];
+        v *= sizeof(T) == 1 ? 0x01010101u : 0x00010001u;
+        *reinterpret_cast<uint4*>(rp + (left ? 0 : BOXW - A)) = make_uint4(v, v, v, v);
+      }
+    } else {
+      const int nc = ncl + ncr;
+      for (int i = lane; i < (y_hi - y_lo) * nc; i += 32) {
+        const int row = y_lo + i / nc, j = i % nc;
+        T* rp = s_in + row * BOXW;
+        rp[j < ncl ? j : c_hi + (j - ncl)] = rp[j < ncl ? c_lo : c_hi - 1];
+      }
+    }
+    __syncwarp();
+  }
+  const int nrt = y_lo, nrb = BOXH - y_hi;
+  constexpr int V = BOXW / A;
+  for (int i = lane; i < (nrt + nrb) * V; i += 32) {
+    const int j = i / V, col = (i - j * V) * A;
+    const int row = j < nrt ? j : y_hi + (j - nrt);
+    *reinterpret_cast<uint4*>(s_in + row * BOXW + col) =
+        *reinterpret_cast<const uint4*>(s_in + (j < nrt ? y_lo : y_hi - 1) * BOXW + col);
+  }
+  __syncwarp();
+}
+
+// Detector over the warp tile (tile::detect_strip with this box geometry).
+template <typename T, int K, bool FULL>
+__device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t pitch, int valid_rows, bool ok0,
+                                       bool ok1, uint32_t (&flags)[2], uint32_t one) {
+  using G = Geo<T, K>;
+  constexpr int r = G::r, BOXW = G::BOXW;
+  constexpr int J = (r + 1) / 2;
+  const uint32_t m1 = 0u - one, k65536 = one << 16, k2p31 = one << 31;
+  uint32_t rmin[K], rmax[K], rcen[r + 1];
+  flags[0] = flags[1] = 0u;
+  const T* rowp = s_in + c0;
+#pragma unroll
+  for (int s = 0; s < WH + 2 * r; ++s) {
+    uint32_t wd[2 * J + 1];
+#pragma unroll
+    for (int j = -J; j <= J; ++j) wd[j + J] = tile::load_pair<T>(rowp + s * BOXW, 2 * j);
+    uint32_t ops[K];
+#pragma unroll
+    for (int d = -r; d <= r; ++d)
+      ops[d + r] = (d & 1) == 0 ? wd[J + d / 2] : shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536);
+    rmin[s % K] = tile::reduce_min<K>(ops);
+    rmax[s % K] = tile::reduce_max<K>(ops);
+    rcen[s % (r + 1)] = wd[J];
+    if (s >= 2 * r) {
+      const int y = s - 2 * r;
+      const uint32_t vmn = tile::reduce_min<K>(rmin), vmx = tile::reduce_max<K>(rmax);
+      const uint32_t c = rcen[(s - r) % (r + 1)];
+      // lane of m == 0 <=> centre is the window min or max (no borrow: vmn <= c <= vmx)
+      const uint32_t m = vmin2(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c));
+      // m <= 0x7FFF per lane, so +0x7FFF sets bit 15 iff m != 0
+      const uint32_t e = fma_add(m, one, 0x7FFF7FFFu);
+      uint32_t sh;
+      asm("mul.hi.u32 %0, %1, %2;" : "=r"(sh) : "r"(flags[y >> 4]), "r"(k2p31));
+      flags[y >> 4] = (sh & 0x7FFF7FFFu) | (~e & 0x80008000u);  // row i ends at bits i / 16 + i
+      if (FULL) tile::store_pair_g<T>(outp, c, true, true);
+      else if (y < valid_rows) tile::store_pair_g<T>(outp, c, ok0, ok1);
+      outp += pitch;
+    }
+  }
+}
+
+// Median of queued pixels (entries y << 8 | x in warp-tile coords), two per lane.
+template <typename T, int K>
+__device__ __forceinline__ uint32_t medians(const T* s_in, const uint16_t* q, int n, T* out_tile, int64_t pitch,
+                                            int lane, bool fnr) {
+  using G = Geo<T, K>;
+  constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
+  uint32_t replaced = 0;
+  for (int i = lane; 2 * i < n; i += 32) {
+    const uint32_t e0 = q[2 * i];
+    const bool two = 2 * i + 1 < n;
+    const uint32_t e1 = two ? q[2 * i + 1] : e0;
+    const int y0 = (int)(e0 >> 8), x0 = (int)(e0 & 0xFFu);
+    const int y1 = (int)(e1 >> 8), x1 = (int)(e1 & 0xFFu);
+    const T* a = s_in + y0 * BOXW + x0 + (R - r);
+    const T* bb = s_in + y1 * BOXW + x1 + (R - r);
+    uint32_t v[K * K];
+#pragma unroll
+    for (int dy = 0; dy < K; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < K; ++dx)
+        v[dy * K + dx] = (uint32_t)a[dy * BOXW + dx] | ((uint32_t)bb[dy * BOXW + dx] << 16);
+    const uint32_t med = tile::median_dispatch<K * K>(v);
+    const uint32_t m0 = med & 0xFFFFu, m1 = med >> 16;
+    out_tile[y0 * pitch + x0] = (T)m0;
+    if (two) out_tile[y1 * pitch + x1] = (T)m1;
+    if (fnr) replaced += (m0 != (uint32_t)a[r * BOXW + r]) + (two && m1 != (uint32_t)bb[r * BOXW + r]);
+  }
+  return replaced;
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant__ CUtensorMap in_map,
+                                                           const tile::TileParams p) {
+  using G = Geo<T, K>;
+  constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((128u - (tile::smem_u32(smem_raw) & 127u)) & 127u);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* wsm = base + warp * G::WARP_BYTES;
+  uint16_t* s_q = reinterpret_cast<uint16_t*>(wsm + G::Q_OFF);
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(wsm + G::BAR_OFF);
+  WTile* s_info = reinterpret_cast<WTile*>(wsm + G::INFO_OFF);
+
+  const int tiles_per_frame = p.tiles_x * p.tiles_y;
+  const int ntiles = tiles_per_frame * p.batch;
+  const bool fnr = p.method == 0;
+  uint32_t replaced = 0, detected = 0;
+
+  // lane 0: grab a warp tile, publish it beside the stage, start its TMA load (or
+  // arrive empty past the end); the mbarrier's release/acquire publishes the info.
+  auto refill = [&](int stage) {
+    WTile ti;
+    ti.t = (int)atomicAdd(p.sched, 1u);
+    if (ti.t < ntiles) {
+      ti.b = ti.t / tiles_per_frame;
+      const int tt = ti.t - ti.b * tiles_per_frame;
+      const int ty = tt / p.tiles_x;
+      ti.x0 = (tt - ty * p.tiles_x) * WW;
+      ti.y0 = p.row_begin + ty * WH;
+      s_info[stage] = ti;
+      tile::mbar_expect_tx(&s_bar[stage], G::IN_BYTES);
+      tile::tma_load_3d(wsm + stage * G::STAGE, &in_map, &s_bar[stage], ti.x0 - R, ti.y0 - r - p.in_row0, ti.b);
+    } else {
+      s_info[stage] = ti;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tile::smem_u32(&s_bar[stage])) : "memory");
+    }
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NSTAGE; ++s) tile::mbar_init(&s_bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < NSTAGE; ++s) refill(s);
+  }
+  __syncwarp();
+
+  const int c0 = 2 * lane + R;  // smem column of this lane's first pixel
+  T* const out_base = reinterpret_cast<T*>(p.out);
+
+  for (int iter = 0;; ++iter) {
+    const int stage = iter % NSTAGE;
+    T* s_in = reinterpret_cast<T*>(wsm + stage * G::STAGE);
+    tile::mbar_wait(&s_bar[stage], (iter / NSTAGE) & 1);
+    const WTile ti = s_info[stage];
+    if (ti.t >= ntiles) break;
+    const int gx_lo = ti.x0 - R, gy_lo = ti.y0 - r;
+    if (gx_lo < 0 || gy_lo < 0 || gx_lo + BOXW > p.width || gy_lo + G::BOXH > p.height)
+      fix_edges_warp<T, K>(s_in, gx_lo, gy_lo, p.width, p.height, lane);
+    const int valid_w = min(WW, p.width - ti.x0);
+    const int valid_h = min(WH, p.row_end - ti.y0);
+    T* const out_tile = out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.y0 - p.row_begin) * p.out_pitch + ti.x0;
+    const bool ok0 = 2 * lane < valid_w, ok1 = 2 * lane + 1 < valid_w;
+    int n;
+    if (fnr) {
+      uint32_t flags[2];
+      T* outp = out_tile + 2 * lane;
+      if (valid_w == WW && valid_h == WH) {
+        detect<T, K, true>(s_in, c0, outp, p.out_pitch, WH, true, true, flags, p.one);
+      } else {
+        detect<T, K, false>(s_in, c0, outp, p.out_pitch, valid_h, ok0, ok1, flags, p.one);
+        const uint32_t colm = (ok0 ? 0xFFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int v = min(16, max(0, valid_h - 16 * h));
+          const uint32_t rowm = v >= 16 ? 0xFFFFu : ((1u << v) - 1u);
+          flags[h] &= colm & (rowm | (rowm << 16));
+        }
+      }
+      const int cnt = __popc(flags[0]) + __popc(flags[1]);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      n = __shfl_sync(0xffffffffu, incl, 31);
+      detected += (uint32_t)cnt;
+      uint16_t* qp = s_q + (incl - cnt);
+      const uint32_t ebase = (uint32_t)(2 * lane);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t f = flags[h];
+        while (f) {
+          const int bit = __ffs(f) - 1;
+          f &= f - 1u;
+          *qp++ = (uint16_t)(ebase + ((uint32_t)(16 * h + (bit & 15)) << 8) + (uint32_t)(bit >> 4));
+        }
+      }
+    } else {
+      const int cols = max(0, valid_w), rows = max(0, valid_h);
+      n = rows * cols;
+      for (int j = lane; j < n; j += 32) {
+        const int y = j / cols, x = j - y * cols;
+        s_q[j] = (uint16_t)((y << 8) | x);
+      }
+    }
+    __syncwarp();  // queue visible; centre stores ordered before the median stores
+    replaced += medians<T, K>(s_in, s_q, n, out_tile, p.out_pitch, lane, fnr);
+    // this stage is free: load the warp's next tile into it
+    tile::fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) refill(stage);
+  }
+  if (lane == 0 && atomicAdd(p.sched + 1, 1u) == gridDim.x * WARPS - 1) {
+    p.sched[0] = 0u;
+    p.sched[1] = 0u;
+  }
+  if (fnr) block_add_counts<THREADS>(detected, replaced, p.counts);
+}
+
+}  // namespace wk
+}  // namespace irdn
