@@ -13,7 +13,8 @@ import os
 import threading
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libirdn.so")
+# IRDN_LIB selects an alternative build of the same library (kernel-variant experiments).
+LIB_PATH = os.environ.get("IRDN_LIB") or os.path.join(PKG_DIR, "libirdn.so")
 SCENE_LIB_PATH = os.path.join(PKG_DIR, "libirdn_scene.so")
 
 IRDN_OK, IRDN_EINVAL, IRDN_ECUDA, IRDN_ENODEV = 0, 1, 2, 3

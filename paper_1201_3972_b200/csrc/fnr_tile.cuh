@@ -373,7 +373,6 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
 #pragma unroll
     for (int s = 0; s < NSTAGE; ++s) mbar_init(&s_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-#pragma unroll
     grab_ahead();
     for (int s = 0; s < NSTAGE; ++s) refill(s);
   }

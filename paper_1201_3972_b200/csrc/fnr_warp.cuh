@@ -23,9 +23,23 @@ namespace wk {
 constexpr int WARPS = 2;               // warps per CTA (packaging only: no CTA barriers)
 constexpr int THREADS = 32 * WARPS;
 constexpr int WW = 64;                 // warp tile width: 32 lanes x 2 pixels
-constexpr int WH = 32;                 // warp tile height
-constexpr int NSTAGE = 2;
-constexpr int QCAP = WW * WH;          // queue entries (every pixel may be noisy)
+#ifndef IRDN_WH
+#define IRDN_WH 32
+#endif
+#ifndef IRDN_DET_FMA
+#define IRDN_DET_FMA 1  // detector adds / shifts as IMADs on the FMA pipe (0: IADD3 / PRMT / SHF)
+#endif
+#ifndef IRDN_WSTAGE
+#define IRDN_WSTAGE 1
+#endif
+constexpr int WH = IRDN_WH;            // warp tile height (16 or 32: one flag word per 16 rows)
+constexpr int NSTAGE = IRDN_WSTAGE;
+#ifndef IRDN_QCAP
+#define IRDN_QCAP 2048
+#endif
+// Queue entries per round: a warp tile with more noisy pixels than QCAP is filtered in
+// several rounds of QCAP pixels (keeps shared memory per warp small -> more warps/SM).
+constexpr int QCAP = IRDN_QCAP;
 
 template <typename T, int K>
 struct Geo {
@@ -92,6 +106,7 @@ __device__ __forceinline__ void fix_edges_warp(T* s_in, int gx_lo, int gy_lo, in
 template <typename T, int K, bool FULL>
 __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t pitch, int valid_rows, bool ok0,
                                        bool ok1, uint32_t (&flags)[2], uint32_t one) {
+  static_assert(WH == 16 || WH == 32, "one or two 16-row flag words");
   using G = Geo<T, K>;
   constexpr int r = G::r, BOXW = G::BOXW;
   constexpr int J = (r + 1) / 2;
@@ -107,7 +122,9 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
     uint32_t ops[K];
 #pragma unroll
     for (int d = -r; d <= r; ++d)
-      ops[d + r] = (d & 1) == 0 ? wd[J + d / 2] : shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536);
+      ops[d + r] = (d & 1) == 0 ? wd[J + d / 2]
+                   : (IRDN_DET_FMA ? shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536)
+                                   : tile::prmt(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], 0x5432u));
     rmin[s % K] = tile::reduce_min<K>(ops);
     rmax[s % K] = tile::reduce_max<K>(ops);
     rcen[s % (r + 1)] = wd[J];
@@ -116,11 +133,12 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
       const uint32_t vmn = tile::reduce_min<K>(rmin), vmx = tile::reduce_max<K>(rmax);
       const uint32_t c = rcen[(s - r) % (r + 1)];
       // lane of m == 0 <=> centre is the window min or max (no borrow: vmn <= c <= vmx)
-      const uint32_t m = vmin2(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c));
+      const uint32_t m = IRDN_DET_FMA ? vmin2(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c)) : vmin2(c - vmn, vmx - c);
       // m <= 0x7FFF per lane, so +0x7FFF sets bit 15 iff m != 0
-      const uint32_t e = fma_add(m, one, 0x7FFF7FFFu);
+      const uint32_t e = IRDN_DET_FMA ? fma_add(m, one, 0x7FFF7FFFu) : m + 0x7FFF7FFFu;
       uint32_t sh;
-      asm("mul.hi.u32 %0, %1, %2;" : "=r"(sh) : "r"(flags[y >> 4]), "r"(k2p31));
+      if (IRDN_DET_FMA) asm("mul.hi.u32 %0, %1, %2;" : "=r"(sh) : "r"(flags[y >> 4]), "r"(k2p31));
+      else sh = flags[y >> 4] >> 1;
       flags[y >> 4] = (sh & 0x7FFF7FFFu) | (~e & 0x80008000u);  // row i ends at bits i / 16 + i
       if (FULL) tile::store_pair_g<T>(outp, c, true, true);
       else if (y < valid_rows) tile::store_pair_g<T>(outp, c, ok0, ok1);
@@ -136,10 +154,18 @@ __device__ __forceinline__ uint32_t medians(const T* s_in, const uint16_t* q, in
   using G = Geo<T, K>;
   constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
   uint32_t replaced = 0;
-  for (int i = lane; 2 * i < n; i += 32) {
-    const uint32_t e0 = q[2 * i];
-    const bool two = 2 * i + 1 < n;
-    const uint32_t e1 = two ? q[2 * i + 1] : e0;
+  // Pair p = (entry p, entry p + P). Lane i takes pairs i*rounds .. i*rounds+rounds-1, so in one round the
+  // 32 lanes touch entries ~n/64 apart: queue order is lane-major (a column pair's noisy
+  // pixels are adjacent), and consecutive entries would hit the same smem banks (TMA rows
+  // are multiples of 16 bytes, so a column's rows share few banks).
+  const int P = (n + 1) >> 1;
+  const int rounds = (P + 31) >> 5;
+  for (int k = 0; k < rounds; ++k) {
+    const int pi = lane * rounds + k;
+    if (pi >= P) break;
+    const uint32_t e0 = q[pi];
+    const bool two = pi + P < n;
+    const uint32_t e1 = two ? q[pi + P] : e0;
     const int y0 = (int)(e0 >> 8), x0 = (int)(e0 & 0xFFu);
     const int y1 = (int)(e1 >> 8), x1 = (int)(e1 & 0xFFu);
     const T* a = s_in + y0 * BOXW + x0 + (R - r);
@@ -237,6 +263,7 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
           flags[h] &= colm & (rowm | (rowm << 16));
         }
       }
+      if (WH == 16) flags[1] = 0u;
       const int cnt = __popc(flags[0]) + __popc(flags[1]);
       int incl = cnt;
 #pragma unroll
@@ -246,27 +273,40 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
       }
       n = __shfl_sync(0xffffffffu, incl, 31);
       detected += (uint32_t)cnt;
-      uint16_t* qp = s_q + (incl - cnt);
+      const int off = incl - cnt;  // index of this lane's first queue entry
       const uint32_t ebase = (uint32_t)(2 * lane);
+      for (int q0 = 0; q0 < n; q0 += QCAP) {
+        if (off < q0 + QCAP && off + cnt > q0) {
+          int idx = off - q0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t f = flags[h];
-        while (f) {
-          const int bit = __ffs(f) - 1;
-          f &= f - 1u;
-          *qp++ = (uint16_t)(ebase + ((uint32_t)(16 * h + (bit & 15)) << 8) + (uint32_t)(bit >> 4));
+          for (int h = 0; h < 2; ++h) {
+            uint32_t f = flags[h];
+            while (f) {
+              const int bit = __ffs(f) - 1;
+              f &= f - 1u;
+              if ((unsigned)idx < (unsigned)QCAP)
+                s_q[idx] = (uint16_t)(ebase + ((uint32_t)(16 * h + (bit & 15)) << 8) + (uint32_t)(bit >> 4));
+              ++idx;
+            }
+          }
         }
+        __syncwarp();  // queue visible; centre stores ordered before the median stores
+        replaced += medians<T, K>(s_in, s_q, min(QCAP, n - q0), out_tile, p.out_pitch, lane, true);
+        __syncwarp();  // queue reads done before the next round overwrites it
       }
     } else {
       const int cols = max(0, valid_w), rows = max(0, valid_h);
       n = rows * cols;
-      for (int j = lane; j < n; j += 32) {
-        const int y = j / cols, x = j - y * cols;
-        s_q[j] = (uint16_t)((y << 8) | x);
+      for (int q0 = 0; q0 < n; q0 += QCAP) {
+        for (int j = lane; j < min(QCAP, n - q0); j += 32) {
+          const int y = (q0 + j) / cols, x = (q0 + j) - y * cols;
+          s_q[j] = (uint16_t)((y << 8) | x);
+        }
+        __syncwarp();
+        medians<T, K>(s_in, s_q, min(QCAP, n - q0), out_tile, p.out_pitch, lane, false);
+        __syncwarp();
       }
     }
-    __syncwarp();  // queue visible; centre stores ordered before the median stores
-    replaced += medians<T, K>(s_in, s_q, n, out_tile, p.out_pitch, lane, fnr);
     // this stage is free: load the warp's next tile into it
     tile::fence_proxy_async();
     __syncwarp();
