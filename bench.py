@@ -153,16 +153,37 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "NVML during the timed region"}
 
 
+_BACKEND = None
+
+
 def dist_setup(n_gpus: int):
+    """One rank per GPU (torchrun). NCCL carries the barrier / max-over-ranks timing; if
+    fewer GPUs than ranks are visible (a code-path check on a 1-GPU box) ranks share GPUs
+    and the control plane falls back to gloo. No data-path collective either way."""
+    global _BACKEND
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=None)
+        ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        _BACKEND = "nccl" if ngpu >= world else "gloo"
+        dist.init_process_group(_BACKEND)
+        if ngpu:
+            local = local % ngpu
     return world, rank, local
+
+
+def _max_over_ranks(value: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device=dev if _BACKEND == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 # ---------------------------------------------------------------------------
@@ -365,9 +386,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+        elapsed_ms = _max_over_ranks(elapsed_ms, dev)
         dist.barrier()
     det = int(counts[0].item())
     ms_per_step = elapsed_ms / steps
@@ -416,11 +435,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
         _native.check(hfn(h_in.data_ptr(), h_out.data_ptr(), B, H, W, cfg.k, 0, 1, local, ctypes.byref(st)))
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = _max_over_ranks(e2e_s, dev)
     e2e = {"value": round(world * batch_px * e2e_steps / e2e_s / 1e6, 3), "unit": "Mpix/s",
            "h2d_bytes_per_step": batch_bytes, "d2h_bytes_per_step": batch_bytes + 16,
            "steps": e2e_steps,

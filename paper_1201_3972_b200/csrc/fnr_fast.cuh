@@ -218,10 +218,10 @@ inline bool use_tile_kernel() {
   return v == 1;
 }
 
-// Dense 3x3 kernel for u8 frames (fnr_k3.cuh).
-inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int method,
-                     unsigned long long* counts, cudaStream_t s, bool* taken) {
-  using G = k3::Geo;
+template <int TH>
+inline int launch_k3_th(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int method,
+                        unsigned long long* counts, cudaStream_t s, bool* taken) {
+  using G = k3::Geo<TH>;
   *taken = false;
   CUtensorMap in_map;
   const int out_rows = g.row_end - g.row_begin;
@@ -231,7 +231,7 @@ inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int
   const bool full_w = g.width % k3::TW == 0;
   static int bps[2] = {0, 0};
   int& blocks_per_sm = bps[full_w ? 1 : 0];
-  auto kern = full_w ? k3::fnr_k3_kernel<true> : k3::fnr_k3_kernel<false>;
+  auto kern = full_w ? k3::fnr_k3_kernel<TH, true> : k3::fnr_k3_kernel<TH, false>;
   if (blocks_per_sm == 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     int n = 0;
@@ -256,12 +256,13 @@ inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int
   p.row_begin = g.row_begin;
   p.row_end = g.row_end;
   p.tiles_x = (g.width + k3::TW - 1) / k3::TW;
-  p.tiles_y = (out_rows + k3::TH - 1) / k3::TH;
+  p.tiles_y = (out_rows + TH - 1) / TH;
   p.batch = g.batch;
   p.method = method;
   p.counts = counts;
   p.sched = sched;
   p.one = 1u;
+  p.debug = 0;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));
@@ -273,6 +274,16 @@ inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int
     return 1;
   }
   return 0;
+}
+
+// Dense 3x3 kernel for u8 frames (fnr_k3.cuh): 128-row tiles, or 32-row tiles when the
+// job has fewer than two 128-row tiles per SM.
+inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int method,
+                     unsigned long long* counts, cudaStream_t s, bool* taken) {
+  const long long tiles128 = (long long)((g.width + k3::TW - 1) / k3::TW) *
+                             ((g.row_end - g.row_begin + 127) / 128) * g.batch;
+  if (tiles128 < 2 * 148) return launch_k3_th<32>(d_in, d_out, g, method, counts, s, taken);
+  return launch_k3_th<128>(d_in, d_out, g, method, counts, s, taken);
 }
 
 template <typename T>

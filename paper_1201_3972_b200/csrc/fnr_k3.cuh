@@ -28,13 +28,14 @@ namespace k3 {
 
 constexpr int THREADS = 128;
 constexpr int TW = 128;                 // tile width (pixels)
-constexpr int TH = 128;                 // tile height (rows)
 constexpr int COLS = 8;                 // columns per thread (one 8-byte row segment)
 constexpr int TPR = TW / COLS;          // threads per row band (16)
 constexpr int BANDS = THREADS / TPR;    // row bands per tile (8)
-constexpr int BAND = TH / BANDS;        // rows per thread (16)
 constexpr int NSTAGE = 2;
+// Tile height: 128 rows (16 per thread) for large frames, 32 rows (4 per thread) when a
+// frame has too few 128-row tiles to fill the GPU (BASELINE c1: 512x512).
 
+template <int TH>
 struct Geo {
   static constexpr int r = 1;
   static constexpr int A = 16;  // TMA box x start must be 16-byte aligned
@@ -55,8 +56,9 @@ __device__ __forceinline__ uint32_t med3(uint32_t a, uint32_t b, uint32_t c, uin
 }
 
 // Replicate-edge fix-up (see tile::fix_edges) for this kernel's box.
+template <int TH>
 __device__ __forceinline__ void fix_edges(uint8_t* s_in, int gx_lo, int gy_lo, int width, int height) {
-  constexpr int BOXW = Geo::BOXW, BOXH = Geo::BOXH, A = Geo::A;
+  constexpr int BOXW = Geo<TH>::BOXW, BOXH = Geo<TH>::BOXH, A = Geo<TH>::A;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c_lo = max(0, -gx_lo), c_hi = min(BOXW, width - gx_lo);
   const int y_lo = max(0, -gy_lo), y_hi = min(BOXH, height - gy_lo);
@@ -94,9 +96,10 @@ __device__ __forceinline__ void fix_edges(uint8_t* s_in, int gx_lo, int gy_lo, i
 }
 
 // Keys of the 10 columns x-1 .. x+8 for smem rows `ra` and `ra + 1` (lane 0 = row ra).
+template <int BOXW>
 __device__ __forceinline__ void load_keys(const uint8_t* s_row, uint32_t (&key)[COLS + 2]) {
   const uint8_t* p1 = s_row;
-  const uint8_t* p2 = s_row + Geo::BOXW;
+  const uint8_t* p2 = s_row + BOXW;
   const uint32_t l1 = *reinterpret_cast<const uint32_t*>(p1 - 4), l2 = *reinterpret_cast<const uint32_t*>(p2 - 4);
   const uint2 m1 = *reinterpret_cast<const uint2*>(p1), m2 = *reinterpret_cast<const uint2*>(p2);
   const uint32_t r1 = *reinterpret_cast<const uint32_t*>(p1 + 8), r2 = *reinterpret_cast<const uint32_t*>(p2 + 8);
@@ -112,10 +115,11 @@ __device__ __forceinline__ void load_keys(const uint8_t* s_row, uint32_t (&key)[
   key[9] = tile::prmt(r1, r2, 0x4400u);  // column x+8 = byte 0 of the right word
 }
 
-template <bool FULL_W>
+template <int TH, bool FULL_W>
 __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__ CUtensorMap in_map,
                                                          const tile::TileParams p) {
-  using G = Geo;
+  using G = Geo<TH>;
+  constexpr int BAND = TH / BANDS;  // rows per thread
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((128u - (tile::smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + G::BAR_OFF);
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
     if (ti.t >= ntiles) break;
     const int gx_lo = ti.tx0 - G::R, gy_lo = ti.ty0 - 1;
     if (gx_lo < 0 || gy_lo < 0 || gx_lo + G::BOXW > p.width || gy_lo + G::BOXH > p.height) {
-      fix_edges(smem + stage * G::IN_STRIDE, gx_lo, gy_lo, p.width, p.height);
+      fix_edges<TH>(smem + stage * G::IN_STRIDE, gx_lo, gy_lo, p.width, p.height);
       __syncthreads();
     }
     const int valid_w = min(TW, p.width - ti.tx0);
@@ -183,12 +187,12 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
     // smem row of output row y is y + 1; the first pair A covers smem rows y0, y0+1
     const uint8_t* srow = s_in + y0 * G::BOXW + x0 + G::R;
     uint32_t A[COLS + 2];
-    load_keys(srow, A);
+    load_keys<G::BOXW>(srow, A);
     uint32_t keep_acc = 0, rep_acc = 0;
-#pragma unroll 2
+#pragma unroll (BAND >= 8 ? 2 : 1)
     for (int s = 0; s < BAND / 2; ++s) {
       uint32_t B[COLS + 2];
-      load_keys(srow + (2 * s + 2) * G::BOXW, B);
+      load_keys<G::BOXW>(srow + (2 * s + 2) * G::BOXW, B);
       uint32_t lo[COLS + 2], hi[COLS + 2], mid[COLS + 2], S[COLS + 2];
 #pragma unroll
       for (int c = 0; c < COLS + 2; ++c) {
