@@ -51,6 +51,13 @@ __device__ __forceinline__ uint32_t shift_pair(uint32_t a, uint32_t b, uint32_t 
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(k65536), "r"(hi));
   return r;
 }
+// PDL: wait for the previous grid in the stream (no-op without PDL), then let the next
+// grid start launching (its CTAs fill SMs this grid has left and wait the same way).
+__device__ __forceinline__ void pdl_wait_and_trigger() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // Block-wide reduction of the two FNR counters followed by ONE 64-bit atomic

@@ -25,6 +25,26 @@ inline uint64_t window_mask(int32_t) {
   return (1ull << 3) | (1ull << 5) | (1ull << 7) | (1ull << 9) | (1ull << 11);
 }
 
+// Launch with programmatic dependent launch (PDL): the next kernel in the stream may be
+// scheduled while this one drains its last tiles; every kernel starts with
+// griddepcontrol.wait (pdl_wait), so it still observes all memory written by the
+// previous kernel before touching global memory — safe for dependent passes.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -142,8 +162,8 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));
   *taken = true;
-  tile::fnr_tile_kernel<T, K><<<grid, tile::THREADS, G::SMEM, s>>>(in_map, p);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(tile::fnr_tile_kernel<T, K>, grid, dim3(tile::THREADS), G::SMEM, s, in_map, p);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_fast_err = cudaGetErrorString(e);
     return 1;
@@ -200,8 +220,8 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   const long long ctas = std::max<long long>(1, std::min<long long>((ntiles + wk::WARPS - 1) / wk::WARPS,
                                                                     (long long)sms * blocks_per_sm));
   *taken = true;
-  wk::fnr_warp_kernel<T, K><<<(unsigned)ctas, wk::THREADS, G::SMEM, s>>>(in_map, p);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(wk::fnr_warp_kernel<T, K>, dim3((unsigned)ctas), dim3(wk::THREADS), G::SMEM, s, in_map, p);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_fast_err = cudaGetErrorString(e);
     return 1;
@@ -267,8 +287,8 @@ inline int launch_k3_th(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, 
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));
   *taken = true;
-  kern<<<grid, k3::THREADS, G::SMEM, s>>>(in_map, p);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(kern, grid, dim3(k3::THREADS), G::SMEM, s, in_map, p);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_fast_err = cudaGetErrorString(e);
     return 1;

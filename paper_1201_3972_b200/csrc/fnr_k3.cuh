@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + G::BAR_OFF);
   tile::TileInfo* s_tile = reinterpret_cast<tile::TileInfo*>(smem + G::TILE_OFF);
 
+  pdl_wait_and_trigger();
   const int tid = threadIdx.x;
   const int tiles_per_frame = p.tiles_x * p.tiles_y;
   const int ntiles = tiles_per_frame * p.batch;

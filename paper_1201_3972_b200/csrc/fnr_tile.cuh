@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + G::BAR_OFF);  // [NSTAGE] stage-full barriers
   TileInfo* s_tile = reinterpret_cast<TileInfo*>(smem + G::TILE_OFF);
 
+  pdl_wait_and_trigger();
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   uint16_t* s_q = reinterpret_cast<uint16_t*>(smem + G::Q_OFF) + warp * STRIP_PX;  // this warp's queue

@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
   constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((128u - (tile::smem_u32(smem_raw) & 127u)) & 127u);
+  pdl_wait_and_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint8_t* wsm = base + warp * G::WARP_BYTES;
   uint16_t* s_q = reinterpret_cast<uint16_t*>(wsm + G::Q_OFF);
