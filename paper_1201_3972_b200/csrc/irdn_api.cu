@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -199,6 +200,7 @@ struct DeviceWorkspace {
   size_t cap = 0;
   unsigned long long* counts = nullptr;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_done;  // grow-only pools (created once, reused per call)
   bool ready = false;
 };
 static DeviceWorkspace g_ws[64];
@@ -256,8 +258,12 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   struct Chunk { int64_t f0, nf, y0, y1; };
   std::vector<Chunk> chunks;
   if (batch >= 2) {
-    const int64_t target = std::max<int64_t>(1, (int64_t)((8u << 20) / sizeof(T)) / frame);  // ~8 MB
-    const int64_t nchunks = std::min<int64_t>(std::max<int64_t>(1, batch / target), 64);
+    static const int64_t chunk_bytes = [] {
+      const char* e = getenv("IRDN_CHUNK_MB");
+      return (int64_t)((e ? atof(e) : 8.0) * (1 << 20));
+    }();
+    const int64_t target = std::max<int64_t>(1, chunk_bytes / (int64_t)sizeof(T) / frame);  // ~8 MB of frames (measured optimum for c2: tools/pcie_probe.py)
+    const int64_t nchunks = std::min<int64_t>(std::max<int64_t>(1, batch / target), 256);
     for (int64_t i = 0; i < nchunks; ++i) {
       int64_t a = batch * i / nchunks, b = batch * (i + 1) / nchunks;
       if (b > a) chunks.push_back({a, b - a, 0, height});
@@ -272,15 +278,15 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
     chunks.push_back({0, batch, 0, height});
   }
 
-  std::vector<cudaEvent_t> ev_in(chunks.size()), ev_done(chunks.size());
-  for (size_t i = 0; i < chunks.size(); ++i) {
-    IRDN_CUDA(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
-    IRDN_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
+  while (ws.ev_in.size() < chunks.size()) {
+    cudaEvent_t a, b;
+    IRDN_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    IRDN_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    ws.ev_in.push_back(a);
+    ws.ev_done.push_back(b);
   }
-  struct EvFree {
-    std::vector<cudaEvent_t>& a; std::vector<cudaEvent_t>& b;
-    ~EvFree() { for (auto e : a) cudaEventDestroy(e); for (auto e : b) cudaEventDestroy(e); }
-  } evfree{ev_in, ev_done};
+  std::vector<cudaEvent_t>& ev_in = ws.ev_in;
+  std::vector<cudaEvent_t>& ev_done = ws.ev_done;
 
   const bool row_mode = batch == 1 && chunks.size() > 1;
   // H2D: each chunk's own rows (row mode: strips, in order).
@@ -317,7 +323,7 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
     IRDN_CUDA(cudaMemcpyAsync(h_out + off, d_out + off, cnt * sizeof(T), cudaMemcpyDeviceToHost, ws.s_d2h));
   }
   unsigned long long counts[2] = {0, 0};
-  IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done.back(), 0));
+  IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[chunks.size() - 1], 0));
   IRDN_CUDA(cudaMemcpyAsync(counts, ws.counts, sizeof(counts), cudaMemcpyDeviceToHost, ws.s_d2h));
   IRDN_CUDA(cudaStreamSynchronize(ws.s_d2h));
   IRDN_CUDA(cudaStreamSynchronize(ws.s_comp));
