@@ -1,12 +1,15 @@
 """Generate exact median-selection networks for the FNR tile kernels.
 
-Algorithm (published, restated): take Batcher's odd-even merge sorting network
-on N = 2^p >= n wires (Knuth TAOCP 5.3.4, Algorithm M), feed the n window
-values plus N-n constants (-inf / +inf split so the median lands on a fixed
-output wire), fold the constants away (a comparator against a constant is
-either a no-op or a wire relabel), then prune backwards: keep only
-comparators whose outputs can reach the median wire, and emit a single
-min or max when only one of a comparator's outputs is live.
+Algorithm (published, restated): take a sorting network on N = 2^p >= n wires —
+Batcher's odd-even merge sort (Knuth TAOCP 5.3.4, Algorithm M) or Parberry's
+pairwise sorting network (1992) — feed the n window values plus N-n constants
+(-inf / +inf placed on chosen wires so the median lands on a fixed output wire),
+fold the constants away (a comparator against a constant is either a no-op or a
+wire relabel), then prune backwards: keep only comparators whose outputs can
+reach the median wire, and emit a single min or max when only one of a
+comparator's outputs is live. Constant placements are searched (seeded random)
+and the network with the fewest instructions after 3-input fusion is kept; the
+pairwise base wins (e.g. 173 vs 192 instructions for 25 inputs).
 
 Each emitted operation is one packed u16x2 min or max (VIMNMX.U16x2 on
 sm_100a), so one network evaluation selects the medians of two windows.
@@ -37,6 +40,110 @@ def oddeven_merge_sort(n: int) -> list[tuple[int, int]]:
             k //= 2
         p *= 2
     return cmps
+
+
+def pairwise_sort(n: int) -> list[tuple[int, int]]:
+    """Parberry's pairwise sorting network for n = 2^p (comparators as (min wire, max wire))."""
+    cmps = []
+    a = 1
+    while a < n:
+        b, c = a, 0
+        while b < n:
+            cmps.append((b - a, b))
+            b += 1
+            c = (c + 1) % a
+            if c == 0:
+                b += a
+        a *= 2
+    a //= 4
+    e = 1
+    while a > 0:
+        d = e
+        while d > 0:
+            b, c = (d + 1) * a, 0
+            while b < n:
+                cmps.append((b - d * a, b))
+                b += 1
+                c = (c + 1) % a
+                if c == 0:
+                    b += a
+            d //= 2
+        a //= 2
+        e = e * 2 + 1
+    return cmps
+
+
+def build_kinds(n: int, rank: int, base, kinds):
+    """Prune `base` (on len(kinds) wires) for the rank-th value; kinds[w] = slot index of a
+    real input, 'L' (-inf) or 'H' (+inf). Returns (ops on real slots, output slot)."""
+    kind = ["R" if isinstance(k, int) else k for k in kinds]
+    k_lo = kind.count("L")
+    live = []
+    for a, b in base:
+        ka, kb = kind[a], kind[b]
+        if ka == "R" and kb == "R":
+            live.append((a, b))
+        elif ka == "L" or kb == "H":
+            continue
+        else:
+            live.append(("swap", a, b))
+            kind[a], kind[b] = kind[b], kind[a]
+    out_wire = rank + k_lo
+    need = {out_wire}
+    kept = []
+    for c in reversed(live):
+        if c[0] == "swap":
+            _, a, b = c
+            need = {b if w == a else a if w == b else w for w in need}
+            kept.append(c)
+            continue
+        a, b = c
+        na, nb = a in need, b in need
+        if na or nb:
+            kept.append(("cx" if (na and nb) else ("min" if na else "max"), a, b))
+            need |= {a, b}
+    kept.reverse()
+    slot = [k if isinstance(k, int) else None for k in kinds]
+    ops = []
+    for c in kept:
+        if c[0] == "swap":
+            _, a, b = c
+            slot[a], slot[b] = slot[b], slot[a]
+            continue
+        op, a, b = c
+        ops.append((op, slot[a], slot[b]))
+    return ops, slot[out_wire]
+
+
+def search(n: int, rank: int, iters: int, seed: int = 1):
+    """Best (fewest fused instructions) network over bases and constant placements."""
+    N = 1
+    while N < n:
+        N *= 2
+    rng = random.Random(seed)
+    best = None
+    for base_fn in (oddeven_merge_sort, pairwise_sort):
+        base = base_fn(N)
+        for it in range(iters):
+            pad = N - n
+            if it == 0:
+                kinds = list(range(n)) + ["L"] * (pad // 2) + ["H"] * (pad - pad // 2)
+            else:
+                k_lo = rng.randint(0, pad)
+                pos = set(rng.sample(range(N), pad))
+                lows = set(rng.sample(sorted(pos), k_lo))
+                kinds, j = [], 0
+                for w in range(N):
+                    if w in pos:
+                        kinds.append("L" if w in lows else "H")
+                    else:
+                        kinds.append(j)
+                        j += 1
+            ops, out = build_kinds(n, rank, base, kinds)
+            cost = len(to_ssa(n, ops, out)[0])
+            if best is None or cost < best[0]:
+                best = (cost, ops, out, base_fn.__name__)
+    return best
 
 
 def build(n: int, rank: int):
@@ -246,11 +353,13 @@ def main():
            "__device__ __forceinline__ uint32_t vmax3(uint32_t a, uint32_t b, uint32_t c) {",
            "  uint32_t r; asm(\"{.reg .b32 t; max.u16x2 t, %1, %2; max.u16x2 %0, t, %3;}\" : \"=r\"(r) : \"r\"(a), \"r\"(b), \"r\"(c)); return r;",
            "}", ""]
+    iters = {9: 400, 25: 1500, 49: 800, 81: 200, 121: 150}
     for n in sizes:
-        cost, ops, slot = build(n, (n - 1) // 2)
+        _, ops, slot, base_name = search(n, (n - 1) // 2, iters.get(n, 100))
         check(n, ops, slot)
+        sys.stderr.write(f"n={n}: base {base_name}\n")
         text = emit(n, ops, slot)
-        sys.stderr.write(f"n={n}: {len(ops)} comparators, {cost} ops -> {text.splitlines()[0]}\n")
+        sys.stderr.write(f"n={n}: {len(ops)} comparators -> {text.splitlines()[0]}\n")
         out.append(text)
         out.append("")
     out.append("}  // namespace irdn")
