@@ -229,13 +229,15 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   return 0;
 }
 
-inline bool use_tile_kernel() {
+// Kernel family for k = 5..11 (and k = 3 on u16): the warp-autonomous kernel; the
+// CTA-tile kernel stays selectable for comparison with IRDN_KERNEL=tile.
+inline int kernel_family() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("IRDN_KERNEL");
-    v = (e && e[0] == 't') ? 1 : 0;
+    v = (e && e[0] == 't') ? 0 : 1;
   }
-  return v == 1;
+  return v;
 }
 
 template <int TH>
@@ -316,23 +318,22 @@ inline bool try_launch(const T* d_in, T* d_out, const PassGeom& g, int k, int me
   if (g.width < 16 || g.height < 1) return false;
   bool taken = false;
   int e = 0;
-  const bool tile_k = use_tile_kernel();
+  const int fam = kernel_family();
+#define IRDN_LAUNCH_K(KK)                                                    \
+  (fam == 0 ? launch_tile<T, KK>(d_in, d_out, g, method, counts, s, &taken) \
+            : launch_warp<T, KK>(d_in, d_out, g, method, counts, s, &taken))
   switch (k) {
     case 3:
       if constexpr (sizeof(T) == 1) e = launch_k3(d_in, d_out, g, method, counts, s, &taken);
-      else e = tile_k ? launch_tile<T, 3>(d_in, d_out, g, method, counts, s, &taken)
-                      : launch_warp<T, 3>(d_in, d_out, g, method, counts, s, &taken);
+      else e = IRDN_LAUNCH_K(3);
       break;
-    case 5: e = tile_k ? launch_tile<T, 5>(d_in, d_out, g, method, counts, s, &taken)
-                       : launch_warp<T, 5>(d_in, d_out, g, method, counts, s, &taken); break;
-    case 7: e = tile_k ? launch_tile<T, 7>(d_in, d_out, g, method, counts, s, &taken)
-                       : launch_warp<T, 7>(d_in, d_out, g, method, counts, s, &taken); break;
-    case 9: e = tile_k ? launch_tile<T, 9>(d_in, d_out, g, method, counts, s, &taken)
-                       : launch_warp<T, 9>(d_in, d_out, g, method, counts, s, &taken); break;
-    case 11: e = tile_k ? launch_tile<T, 11>(d_in, d_out, g, method, counts, s, &taken)
-                        : launch_warp<T, 11>(d_in, d_out, g, method, counts, s, &taken); break;
+    case 5: e = IRDN_LAUNCH_K(5); break;
+    case 7: e = IRDN_LAUNCH_K(7); break;
+    case 9: e = IRDN_LAUNCH_K(9); break;
+    case 11: e = IRDN_LAUNCH_K(11); break;
     default: return false;
   }
+#undef IRDN_LAUNCH_K
   if (!taken) return false;
   *rc = e ? 2 : 0;
   return true;

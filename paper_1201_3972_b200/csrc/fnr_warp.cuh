@@ -63,10 +63,10 @@ struct WTile {
 };
 
 // replicate-edge fix-up of one warp's box (cells outside the frame)
-template <typename T, int K>
+template <typename T, int K, int BOXW = Geo<T, K>::BOXW, int BOXH = Geo<T, K>::BOXH>
 __device__ __forceinline__ void fix_edges_warp(T* s_in, int gx_lo, int gy_lo, int width, int height, int lane) {
   using G = Geo<T, K>;
-  constexpr int BOXW = G::BOXW, BOXH = G::BOXH, A = G::A;
+  constexpr int A = G::A;
   const int c_lo = max(0, -gx_lo), c_hi = min(BOXW, width - gx_lo);
   const int y_lo = max(0, -gy_lo), y_hi = min(BOXH, height - gy_lo);
   const int ncl = c_lo, ncr = BOXW - c_hi;
@@ -192,7 +192,6 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
   constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((128u - (tile::smem_u32(smem_raw) & 127u)) & 127u);
-  pdl_wait_and_trigger();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint8_t* wsm = base + warp * G::WARP_BYTES;
   uint16_t* s_q = reinterpret_cast<uint16_t*>(wsm + G::Q_OFF);
@@ -206,9 +205,9 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
 
   // lane 0: grab a warp tile, publish it beside the stage, start its TMA load (or
   // arrive empty past the end); the mbarrier's release/acquire publishes the info.
-  auto refill = [&](int stage) {
+  auto refill = [&](int stage, int pre = -1) {
     WTile ti;
-    ti.t = (int)atomicAdd(p.sched, 1u);
+    ti.t = pre >= 0 ? pre : (int)atomicAdd(p.sched, 1u);
     if (ti.t < ntiles) {
       ti.b = ti.t / tiles_per_frame;
       const int tt = ti.t - ti.b * tiles_per_frame;
@@ -223,12 +222,28 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tile::smem_u32(&s_bar[stage])) : "memory");
     }
   };
+  // Before waiting for the previous grid (PDL): take the first tile and pull it into L2.
+  // A prefetch is only a hint (L2 stays coherent with the previous grid's writes), so it
+  // is safe even when that grid produces this kernel's input; the smem load itself is
+  // issued after griddepcontrol.wait.
+  int first = 0;
+  if (lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&in_map) : "memory");
+    first = (int)atomicAdd(p.sched, 1u);
+    if (first < ntiles) {
+      const int b = first / tiles_per_frame, tt = first - b * tiles_per_frame, ty = tt / p.tiles_x;
+      asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(&in_map),
+                   "r"((tt - ty * p.tiles_x) * WW - R), "r"(p.row_begin + ty * WH - r - p.in_row0), "r"(b)
+                   : "memory");
+    }
+  }
+  pdl_wait_and_trigger();
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < NSTAGE; ++s) tile::mbar_init(&s_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
-    for (int s = 0; s < NSTAGE; ++s) refill(s);
+    for (int s = 0; s < NSTAGE; ++s) refill(s, s == 0 ? first : -1);
   }
   __syncwarp();
 
