@@ -94,9 +94,11 @@ inline bool make_map(CUtensorMap* map, const void* base, int64_t width, int64_t 
 // Each launch takes the next slot round-robin; a slot returns to {0, 0} when the
 // launch using it finishes, so up to kSlots launches may be in flight at once.
 constexpr int kSchedSlots = 256;
+inline unsigned int* g_sched_pool[64] = {nullptr};
+inline unsigned int* sched_slot_base(int dev) { return g_sched_pool[dev]; }
 inline unsigned int* sched_slot(int dev) {
   static std::mutex mu;
-  static unsigned int* pool[64] = {nullptr};
+  static unsigned int** pool = g_sched_pool;
   static unsigned int next[64] = {0};
   if (dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
@@ -112,6 +114,30 @@ inline unsigned int* sched_slot(int dev) {
   }
   const unsigned int slot = next[dev]++ % kSchedSlots;
   return pool[dev] + slot * 32;
+}
+
+// Overflow lists of the warp kernel (fnr_warp.cuh), one per scheduler slot.
+constexpr int kOvCap = 16384;  // entries per launch
+inline unsigned long long* ov_slot(int dev, const unsigned int* sched) {
+  static std::mutex mu;
+  static unsigned long long* pool[64] = {nullptr};
+  static unsigned int* sched_base[64] = {nullptr};
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pool[dev]) {
+    void* p = nullptr;
+    const size_t bytes = (size_t)kSchedSlots * kOvCap * sizeof(unsigned long long);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    cudaMemset(p, 0, bytes);
+    cudaDeviceSynchronize();
+    pool[dev] = static_cast<unsigned long long*>(p);
+    sched_base[dev] = sched_slot_base(dev);
+  }
+  const size_t slot = (size_t)(sched - sched_base[dev]) / 32;
+  return pool[dev] + slot * kOvCap;
 }
 
 template <typename T, int K>
@@ -158,6 +184,9 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.sched = sched;
   p.one = 1u;
   p.debug = getenv("IRDN_DEBUG") ? atoi(getenv("IRDN_DEBUG")) : 0;
+  p.full_tiles = 0;
+  p.ov_keep = 0;
+  p.debug_buf = nullptr;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));
@@ -170,6 +199,11 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   }
   return 0;
 }
+
+#ifdef IRDN_TIMELINE
+// Experiments only: per-tile (wait, ready, detected, done, n, warp << 16 | smid) of the last warp-kernel launch.
+inline unsigned long long* g_timeline = nullptr;
+#endif
 
 // Warp-autonomous kernel (fnr_warp.cuh): 64 x 32 warp tiles, per-warp TMA ring.
 template <typename T, int K>
@@ -215,10 +249,30 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.sched = sched;
   p.one = 1u;
   p.debug = 0;
+  p.debug_buf = nullptr;
+#ifdef IRDN_TIMELINE
+  if (!g_timeline) cudaMalloc(&g_timeline, 8 << 20);
+  cudaMemsetAsync(g_timeline, 0, 8 << 20, s);
+  p.debug_buf = g_timeline;
+#endif
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
-  if (ntiles > 0x7fffffffLL) return 0;
+  if (2 * ntiles > 0x7fffffffLL) return 0;
   const long long ctas = std::max<long long>(1, std::min<long long>((ntiles + wk::WARPS - 1) / wk::WARPS,
                                                                     (long long)sms * blocks_per_sm));
+  // Tail: the last `split` full tiles are handed out as two half-height tiles each
+  // (about one tile per warp; none when the pool is a single wave).
+  static const double tail_waves = getenv("IRDN_TAIL") ? atof(getenv("IRDN_TAIL")) : 1.0;
+  long long split = wk::WH == 32 ? (long long)(tail_waves * ctas * wk::WARPS) : 0;
+  if (ntiles <= ctas * wk::WARPS) split = 0;
+  split = std::min(split, ntiles);
+  p.full_tiles = (int)(ntiles - split);
+  static const int ov_keep = getenv("IRDN_OVKEEP") ? atoi(getenv("IRDN_OVKEEP")) : 0;
+  p.ov = method == 0 && ov_keep > 0 ? ov_slot(dev, sched) : nullptr;
+  p.ov_keep = p.ov ? ov_keep : 0;
+  p.ov_cap = kOvCap;
+  p.in = d_in;
+  p.in_pitch = g.in_pitch;
+  p.in_frame = g.in_frame_stride;
   *taken = true;
   cudaError_t e = launch_pdl(wk::fnr_warp_kernel<T, K>, dim3((unsigned)ctas), dim3(wk::THREADS), G::SMEM, s, in_map, p);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -285,6 +339,9 @@ inline int launch_k3_th(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, 
   p.sched = sched;
   p.one = 1u;
   p.debug = 0;
+  p.full_tiles = 0;
+  p.ov_keep = 0;
+  p.debug_buf = nullptr;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));

@@ -54,13 +54,36 @@ struct Geo {
   static constexpr int Q_OFF = NSTAGE * STAGE;
   static constexpr int BAR_OFF = Q_OFF + QCAP * 2;
   static constexpr int INFO_OFF = BAR_OFF + 8 * NSTAGE;
-  static constexpr int WARP_BYTES = (INFO_OFF + 16 * NSTAGE + 127) & ~127;
+  static constexpr int WARP_BYTES = (INFO_OFF + 32 * NSTAGE + 127) & ~127;
   static constexpr int SMEM = WARPS * WARP_BYTES + 128;
 };
 
 struct WTile {
-  int t, b, x0, y0;
+  int t, b, x0, y0, rows;
 };
+
+// Tile t of the pass. The pool ends in half-height tiles (the halves of the last
+// ntiles - full_tiles full tiles, p.full_tiles.. onwards), so the warps that finish
+// last finish a short tile: with ~3.5 tiles per warp the tail of a 64 x 32 pool is
+// about one tile time.
+__device__ __forceinline__ WTile tile_of(const tile::TileParams& p, int t, int tiles_per_frame) {
+  WTile ti;
+  ti.t = t;
+  int f = t, rows = WH, dy = 0;
+  if (t >= p.full_tiles) {
+    const int h = t - p.full_tiles;
+    f = p.full_tiles + (h >> 1);
+    rows = WH / 2;
+    dy = (h & 1) * (WH / 2);
+  }
+  ti.b = f / tiles_per_frame;
+  const int tt = f - ti.b * tiles_per_frame;
+  const int ty = tt / p.tiles_x;
+  ti.x0 = (tt - ty * p.tiles_x) * WW;
+  ti.y0 = p.row_begin + ty * WH + dy;
+  ti.rows = rows;
+  return ti;
+}
 
 // replicate-edge fix-up of one warp's box (cells outside the frame)
 template <typename T, int K, int BOXW = Geo<T, K>::BOXW, int BOXH = Geo<T, K>::BOXH>
@@ -103,7 +126,7 @@ __device__ __forceinline__ void fix_edges_warp(T* s_in, int gx_lo, int gy_lo, in
 }
 
 // Detector over the warp tile (tile::detect_strip with this box geometry).
-template <typename T, int K, bool FULL>
+template <typename T, int K, bool FULL, int ROWS = WH>
 __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t pitch, int valid_rows, bool ok0,
                                        bool ok1, uint32_t (&flags)[2], uint32_t one) {
   static_assert(WH == 16 || WH == 32, "one or two 16-row flag words");
@@ -115,7 +138,7 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
   flags[0] = flags[1] = 0u;
   const T* rowp = s_in + c0;
 #pragma unroll
-  for (int s = 0; s < WH + 2 * r; ++s) {
+  for (int s = 0; s < ROWS + 2 * r; ++s) {
     uint32_t wd[2 * J + 1];
 #pragma unroll
     for (int j = -J; j <= J; ++j) wd[j + J] = tile::load_pair<T>(rowp + s * BOXW, 2 * j);
@@ -185,6 +208,100 @@ __device__ __forceinline__ uint32_t medians(const T* s_in, const uint16_t* q, in
   return replaced;
 }
 
+// ---- overflow list (heavy tiles) ---------------------------------------------
+// A warp tile with far more noisy pixels than usual (clusters of hot pixels / sharp
+// texture: up to ~70 % of a tile vs ~8 % typical on c2) takes 5-10x the median time of
+// a normal tile and, picked up late, ends the launch on its own. Such a warp keeps the
+// first ov_keep queue entries and publishes the rest (tile index << 16 | entry, tag bit
+// 63) to a per-launch global list; warps that find the tile pool empty drain the list
+// before they exit, reading the windows straight from the input (in L2).
+//
+// List accounting is one 64-bit word (sched[2..3]: claimed in the low half, reserved in
+// the high half), so a reservation and a claim are each a single atomicAdd and each
+// sees the other's counter exactly:
+//   * claim: atomicAdd(word, 64) -> (rsv, clm); the claimer processes
+//     [clm, min(clm + 64, rsv, cap)). Slots past rsv are "phantom-claimed";
+//   * reserve: atomicAdd(word, g << 32) -> (rsv, clm); slots of [rsv, rsv + g) below
+//     clm were phantom-claimed by a warp that will not process them, and slots at or past
+//     cap do not exist, so the owner publishes only [max(rsv, clm), min(rsv + g, cap))
+//     and keeps the rest in its local queue;
+//   * an owner claims until the list is empty before it exits, so every published entry
+//     is claimed by a running warp; other warps may leave as soon as a read shows the
+//     list empty.
+constexpr unsigned long long kOvTag = 1ull << 63;
+
+__device__ __forceinline__ void ov_publish(unsigned long long* ptr, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(ptr), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ov_take(unsigned long long* ptr) {
+  unsigned long long v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ptr) : "memory");
+    if (v & kOvTag) break;
+    __nanosleep(32);
+  }
+  *ptr = 0ull;  // the list is clean again for the next launch that uses this slot
+  return v;
+}
+
+template <typename T, int K>
+__device__ __forceinline__ uint32_t ov_drain(const tile::TileParams& p, int tiles_per_frame, int lane,
+                                             bool owner) {
+  constexpr int r = K / 2;
+  const T* in = reinterpret_cast<const T*>(p.in);
+  T* out = reinterpret_cast<T*>(p.out);
+  unsigned long long* word = reinterpret_cast<unsigned long long*>(p.sched + 2);
+  uint32_t replaced = 0;
+  for (;;) {
+    unsigned long long w = 0ull;
+    if (lane == 0) {
+      w = *reinterpret_cast<volatile unsigned long long*>(word);
+      const unsigned int rsv0 = (unsigned int)(w >> 32), clm0 = (unsigned int)w;
+      if (owner || clm0 < min(rsv0, (unsigned)p.ov_cap)) w = atomicAdd(word, 64ull);
+    }
+    w = __shfl_sync(0xffffffffu, w, 0);
+    const unsigned int rsv = min((unsigned int)(w >> 32), (unsigned)p.ov_cap), c0 = (unsigned int)w;
+    if (c0 >= rsv) break;
+    const unsigned int take = min(64u, rsv - c0);
+    if ((unsigned)lane < take) {
+      const bool two = (unsigned)lane + 32u < take;
+      const unsigned long long e0 = ov_take(p.ov + c0 + lane);
+      const unsigned long long e1 = two ? ov_take(p.ov + c0 + lane + 32) : e0;
+      int ys[2], xs[2], bs[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const unsigned long long e = h ? e1 : e0;
+        const WTile ti = tile_of(p, (int)((e & ~kOvTag) >> 16), tiles_per_frame);
+        ys[h] = ti.y0 + (int)((e >> 8) & 0xFFu);
+        xs[h] = ti.x0 + (int)(e & 0xFFu);
+        bs[h] = ti.b;
+      }
+      const T* f0 = in + (int64_t)bs[0] * p.in_frame;
+      const T* f1 = in + (int64_t)bs[1] * p.in_frame;
+      uint32_t v[K * K];
+#pragma unroll
+      for (int dy = 0; dy < K; ++dy) {
+        const T* r0 = f0 + (int64_t)(clampi(ys[0] + dy - r, 0, p.height - 1) - p.in_row0) * p.in_pitch;
+        const T* r1 = f1 + (int64_t)(clampi(ys[1] + dy - r, 0, p.height - 1) - p.in_row0) * p.in_pitch;
+#pragma unroll
+        for (int dx = 0; dx < K; ++dx)
+          v[dy * K + dx] = (uint32_t)r0[clampi(xs[0] + dx - r, 0, p.width - 1)] |
+                           ((uint32_t)r1[clampi(xs[1] + dx - r, 0, p.width - 1)] << 16);
+      }
+      const uint32_t c = v[r * K + r];
+      const uint32_t med = tile::median_dispatch<K * K>(v);
+      out[(int64_t)bs[0] * p.out_frame + (int64_t)(ys[0] - p.row_begin) * p.out_pitch + xs[0]] = (T)(med & 0xFFFFu);
+      replaced += (med & 0xFFFFu) != (c & 0xFFFFu);
+      if (two) {
+        out[(int64_t)bs[1] * p.out_frame + (int64_t)(ys[1] - p.row_begin) * p.out_pitch + xs[1]] = (T)(med >> 16);
+        replaced += (med >> 16) != (c >> 16);
+      }
+    }
+  }
+  return replaced;
+}
+
 template <typename T, int K>
 __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant__ CUtensorMap in_map,
                                                            const tile::TileParams p) {
@@ -199,21 +316,18 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
   WTile* s_info = reinterpret_cast<WTile*>(wsm + G::INFO_OFF);
 
   const int tiles_per_frame = p.tiles_x * p.tiles_y;
-  const int ntiles = tiles_per_frame * p.batch;
+  const int ntiles = p.full_tiles + 2 * (tiles_per_frame * p.batch - p.full_tiles);
   const bool fnr = p.method == 0;
   uint32_t replaced = 0, detected = 0;
 
   // lane 0: grab a warp tile, publish it beside the stage, start its TMA load (or
   // arrive empty past the end); the mbarrier's release/acquire publishes the info.
   auto refill = [&](int stage, int pre = -1) {
+    const int t = pre >= 0 ? pre : (int)atomicAdd(p.sched, 1u);
     WTile ti;
-    ti.t = pre >= 0 ? pre : (int)atomicAdd(p.sched, 1u);
-    if (ti.t < ntiles) {
-      ti.b = ti.t / tiles_per_frame;
-      const int tt = ti.t - ti.b * tiles_per_frame;
-      const int ty = tt / p.tiles_x;
-      ti.x0 = (tt - ty * p.tiles_x) * WW;
-      ti.y0 = p.row_begin + ty * WH;
+    ti.t = t;
+    if (t < ntiles) {
+      ti = tile_of(p, t, tiles_per_frame);
       s_info[stage] = ti;
       tile::mbar_expect_tx(&s_bar[stage], G::IN_BYTES);
       tile::tma_load_3d(wsm + stage * G::STAGE, &in_map, &s_bar[stage], ti.x0 - R, ti.y0 - r - p.in_row0, ti.b);
@@ -231,9 +345,9 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
     asm volatile("prefetch.tensormap [%0];" ::"l"(&in_map) : "memory");
     first = (int)atomicAdd(p.sched, 1u);
     if (first < ntiles) {
-      const int b = first / tiles_per_frame, tt = first - b * tiles_per_frame, ty = tt / p.tiles_x;
+      const WTile f = tile_of(p, first, tiles_per_frame);
       asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(&in_map),
-                   "r"((tt - ty * p.tiles_x) * WW - R), "r"(p.row_begin + ty * WH - r - p.in_row0), "r"(b)
+                   "r"(f.x0 - R), "r"(f.y0 - r - p.in_row0), "r"(f.b)
                    : "memory");
     }
   }
@@ -248,19 +362,35 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
   __syncwarp();
 
   const int c0 = 2 * lane + R;  // smem column of this lane's first pixel
+  bool owner = false;           // this warp published overflow entries (drains until the list is empty)
   T* const out_base = reinterpret_cast<T*>(p.out);
 
+#ifdef IRDN_TIMELINE
+  uint64_t t_wait, t_ready, t_det = 0, t_done;
+#define IRDN_TL_NOW(v) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
+#endif
   for (int iter = 0;; ++iter) {
     const int stage = iter % NSTAGE;
     T* s_in = reinterpret_cast<T*>(wsm + stage * G::STAGE);
+#ifdef IRDN_TIMELINE
+    IRDN_TL_NOW(t_wait);
+#endif
     tile::mbar_wait(&s_bar[stage], (iter / NSTAGE) & 1);
     const WTile ti = s_info[stage];
     if (ti.t >= ntiles) break;
+#ifdef IRDN_TIMELINE
+    IRDN_TL_NOW(t_ready);
+#endif
+    const int valid_w = min(WW, p.width - ti.x0);
+    const int valid_h = min(ti.rows, p.row_end - ti.y0);
+    if (valid_h <= 0) {  // lower half of a bottom-edge tile with <= WH / 2 rows
+      __syncwarp();
+      if (lane == 0) refill(stage);
+      continue;
+    }
     const int gx_lo = ti.x0 - R, gy_lo = ti.y0 - r;
     if (gx_lo < 0 || gy_lo < 0 || gx_lo + BOXW > p.width || gy_lo + G::BOXH > p.height)
       fix_edges_warp<T, K>(s_in, gx_lo, gy_lo, p.width, p.height, lane);
-    const int valid_w = min(WW, p.width - ti.x0);
-    const int valid_h = min(WH, p.row_end - ti.y0);
     T* const out_tile = out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.y0 - p.row_begin) * p.out_pitch + ti.x0;
     const bool ok0 = 2 * lane < valid_w, ok1 = 2 * lane + 1 < valid_w;
     int n;
@@ -269,6 +399,9 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
       T* outp = out_tile + 2 * lane;
       if (valid_w == WW && valid_h == WH) {
         detect<T, K, true>(s_in, c0, outp, p.out_pitch, WH, true, true, flags, p.one);
+      } else if (WH == 32 && valid_w == WW && valid_h == WH / 2 && ti.rows == WH / 2) {
+        detect<T, K, true, WH / 2>(s_in, c0, outp, p.out_pitch, WH / 2, true, true, flags, p.one);
+        flags[1] = 0u;
       } else {
         detect<T, K, false>(s_in, c0, outp, p.out_pitch, valid_h, ok0, ok1, flags, p.one);
         const uint32_t colm = (ok0 ? 0xFFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
@@ -280,6 +413,9 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
         }
       }
       if (WH == 16) flags[1] = 0u;
+#ifdef IRDN_TIMELINE
+      IRDN_TL_NOW(t_det);
+#endif
       const int cnt = __popc(flags[0]) + __popc(flags[1]);
       int incl = cnt;
 #pragma unroll
@@ -291,8 +427,65 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
       detected += (uint32_t)cnt;
       const int off = incl - cnt;  // index of this lane's first queue entry
       const uint32_t ebase = (uint32_t)(2 * lane);
-      for (int q0 = 0; q0 < n; q0 += QCAP) {
-        if (off < q0 + QCAP && off + cnt > q0) {
+      // published entries: queue indices [lo, hi), at list slot ovb + (idx - lo)
+      int lo = 0, hi = 0, ovb = 0;
+      if (n > p.ov_keep && p.ov_keep > 0) {
+        if (lane == 0) {
+          const unsigned long long w0 = *reinterpret_cast<volatile unsigned long long*>(p.sched + 2);
+          const int g = min(n - p.ov_keep, p.ov_cap - (int)min((unsigned)(w0 >> 32), (unsigned)p.ov_cap));
+          if (g > 0) {
+            const unsigned long long w =
+                atomicAdd(reinterpret_cast<unsigned long long*>(p.sched + 2), (unsigned long long)g << 32);
+            const long long rsv = (long long)(w >> 32), clm = (long long)(unsigned int)w;
+            const long long pub0 = max(rsv, clm), pub1 = min(rsv + g, (long long)p.ov_cap);
+            if (pub1 > pub0) {
+              lo = p.ov_keep + (int)(pub0 - rsv);
+              hi = p.ov_keep + (int)(pub1 - rsv);
+              ovb = (int)pub0;
+            }
+          }
+        }
+        lo = __shfl_sync(0xffffffffu, lo, 0);
+        hi = __shfl_sync(0xffffffffu, hi, 0);
+        ovb = __shfl_sync(0xffffffffu, ovb, 0);
+        if (hi > lo) owner = true;
+        if (hi > lo && off + cnt > lo && off < hi) {
+          __threadfence();
+          int idx = off;
+          const unsigned long long tbits = kOvTag | ((unsigned long long)ti.t << 16);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t f = flags[h];
+            while (f) {
+              const int bit = __ffs(f) - 1;
+              f &= f - 1u;
+              if (idx >= lo && idx < hi)
+                ov_publish(p.ov + ovb + (idx - lo),
+                           tbits | (ebase + ((uint32_t)(16 * h + (bit & 15)) << 8) + (uint32_t)(bit >> 4)));
+              ++idx;
+            }
+          }
+        }
+      }
+      const int granted = hi - lo;
+      // local queue: entries [0, lo) and [hi, n), renumbered contiguously
+      const int nl = n - granted;
+      for (int q0 = 0; q0 < nl; q0 += QCAP) {
+        if (granted > 0) {
+          int idx = off;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t f = flags[h];
+            while (f) {
+              const int bit = __ffs(f) - 1;
+              f &= f - 1u;
+              const int li = idx < lo ? idx : idx - granted;
+              if ((idx < lo || idx >= hi) && (unsigned)(li - q0) < (unsigned)QCAP)
+                s_q[li - q0] = (uint16_t)(ebase + ((uint32_t)(16 * h + (bit & 15)) << 8) + (uint32_t)(bit >> 4));
+              ++idx;
+            }
+          }
+        } else if (off < q0 + QCAP && off + cnt > q0) {
           int idx = off - q0;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -307,7 +500,7 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
           }
         }
         __syncwarp();  // queue visible; centre stores ordered before the median stores
-        replaced += medians<T, K>(s_in, s_q, min(QCAP, n - q0), out_tile, p.out_pitch, lane, true);
+        replaced += medians<T, K>(s_in, s_q, min(QCAP, nl - q0), out_tile, p.out_pitch, lane, true);
         __syncwarp();  // queue reads done before the next round overwrites it
       }
     } else {
@@ -323,14 +516,45 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
         __syncwarp();
       }
     }
+#ifdef IRDN_TIMELINE
+    IRDN_TL_NOW(t_done);
+    if (lane == 0 && p.debug_buf) {
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      unsigned long long* d = p.debug_buf + (size_t)ti.t * 6;
+      d[0] = t_wait;
+      d[1] = t_ready;
+      d[2] = t_det;
+      d[3] = t_done;
+      d[4] = (unsigned long long)n;
+      d[5] = ((unsigned long long)(blockIdx.x * WARPS + warp) << 16) | smid;
+    }
+#endif
     // this stage is free: load the warp's next tile into it
     tile::fence_proxy_async();
     __syncwarp();
     if (lane == 0) refill(stage);
   }
+#ifdef IRDN_TIMELINE
+  uint64_t t_d0, t_d1;
+  IRDN_TL_NOW(t_d0);
+#endif
+  if (fnr && p.ov_keep > 0) replaced += ov_drain<T, K>(p, tiles_per_frame, lane, owner);
+#ifdef IRDN_TIMELINE
+  IRDN_TL_NOW(t_d1);
+  if (lane == 0 && p.debug_buf) {
+    unsigned long long* d = p.debug_buf + 600000 + (size_t)(blockIdx.x * WARPS + warp) * 4;
+    d[0] = t_d0;
+    d[1] = t_d1;
+    d[2] = owner;
+    d[3] = 1;
+  }
+#endif
   if (lane == 0 && atomicAdd(p.sched + 1, 1u) == gridDim.x * WARPS - 1) {
     p.sched[0] = 0u;
     p.sched[1] = 0u;
+    p.sched[2] = 0u;
+    p.sched[3] = 0u;
   }
   if (fnr) block_add_counts<THREADS>(detected, replaced, p.counts);
 }

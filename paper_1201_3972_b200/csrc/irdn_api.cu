@@ -434,4 +434,11 @@ int32_t irdn_set_force_generic(int32_t on) {
   return prev;
 }
 
+#ifdef IRDN_TIMELINE
+IRDN_API int irdn_debug_timeline(void* host, int64_t bytes) {
+  if (!irdn::fast::g_timeline) return IRDN_EINVAL;
+  return cudaMemcpy(host, irdn::fast::g_timeline, std::min<int64_t>(bytes, 8 << 20), cudaMemcpyDeviceToHost) ==
+                 cudaSuccess ? IRDN_OK : IRDN_ECUDA;
+}
+#endif
 }  // extern "C"

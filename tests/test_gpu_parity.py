@@ -238,3 +238,34 @@ def test_single_frame_row_pipeline(cuda_ok):
     assert gst == counters(dst)
     rows, _ = oracle.filter_rows_c(img, 11, 1020, 1030)
     assert np.array_equal(got[1020:1030], rows)
+
+
+@pytest.mark.parametrize("dtype,k", [(np.uint16, 5), (np.uint8, 7), (np.uint16, 11)])
+def test_heavy_tiles_overflow_list(cuda_ok, dtype, k):
+    """Warp tiles with far more noisy pixels than ov_keep hand the excess to the overflow
+    list (fnr_warp.cuh); with the whole batch heavy the list also fills up (kOvCap) and
+    the rest stays with the owning warp. Both must match the oracle bit for bit, whole
+    frames and row strips (input rows offset from the frame)."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    smooth = CONFIGS["c2"].with_shape(height=200, width=330)
+    img = generate(smooth, nframes=12).astype(dtype)
+    img[3:9, 40:140, 64:200] = rng.integers(0, 3, size=(6, 100, 136)).astype(dtype)  # heavy patches
+    img[10] = rng.integers(0, 2, size=img[10].shape).astype(dtype)  # a whole heavy frame
+    want, wst = _oracle(img, k, "fnr", 1)
+    got, gst = gpu_filter(img, k, "fnr", 1)
+    assert np.array_equal(got, want) and gst == wst
+    heavy = rng.integers(0, 4, size=(48, 256, 320)).astype(dtype)  # ~all flagged: list overflows
+    want, wst = _oracle(heavy, k, "fnr", 1)
+    got, gst = gpu_filter(heavy, k, "fnr", 1)
+    assert np.array_equal(got, want) and gst == wst
+    t = torch.from_numpy(img[10]).cuda()
+    whole, st = P.run_filter(t, P.WindowSpec(k), "fnr", 1)
+    parts, det = [], 0
+    for a, b in ((0, 37), (37, 120), (120, 200)):
+        o, (d, _) = _strip_call(t, k, a, b)
+        parts.append(o)
+        det += d
+    assert torch.equal(as_i32(torch.cat(parts)), as_i32(whole)) and det == st.detected
+    assert np.array_equal(as_i32(whole).cpu().numpy().astype(dtype), _oracle(img[10], k)[0])
