@@ -94,11 +94,9 @@ inline bool make_map(CUtensorMap* map, const void* base, int64_t width, int64_t 
 // Each launch takes the next slot round-robin; a slot returns to {0, 0} when the
 // launch using it finishes, so up to kSlots launches may be in flight at once.
 constexpr int kSchedSlots = 256;
-inline unsigned int* g_sched_pool[64] = {nullptr};
-inline unsigned int* sched_slot_base(int dev) { return g_sched_pool[dev]; }
 inline unsigned int* sched_slot(int dev) {
   static std::mutex mu;
-  static unsigned int** pool = g_sched_pool;
+  static unsigned int* pool[64] = {nullptr};
   static unsigned int next[64] = {0};
   if (dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
@@ -114,30 +112,6 @@ inline unsigned int* sched_slot(int dev) {
   }
   const unsigned int slot = next[dev]++ % kSchedSlots;
   return pool[dev] + slot * 32;
-}
-
-// Overflow lists of the warp kernel (fnr_warp.cuh), one per scheduler slot.
-constexpr int kOvCap = 16384;  // entries per launch
-inline unsigned long long* ov_slot(int dev, const unsigned int* sched) {
-  static std::mutex mu;
-  static unsigned long long* pool[64] = {nullptr};
-  static unsigned int* sched_base[64] = {nullptr};
-  if (dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (!pool[dev]) {
-    void* p = nullptr;
-    const size_t bytes = (size_t)kSchedSlots * kOvCap * sizeof(unsigned long long);
-    if (cudaMalloc(&p, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return nullptr;
-    }
-    cudaMemset(p, 0, bytes);
-    cudaDeviceSynchronize();
-    pool[dev] = static_cast<unsigned long long*>(p);
-    sched_base[dev] = sched_slot_base(dev);
-  }
-  const size_t slot = (size_t)(sched - sched_base[dev]) / 32;
-  return pool[dev] + slot * kOvCap;
 }
 
 template <typename T, int K>
@@ -185,7 +159,6 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.one = 1u;
   p.debug = getenv("IRDN_DEBUG") ? atoi(getenv("IRDN_DEBUG")) : 0;
   p.full_tiles = 0;
-  p.ov_keep = 0;
   p.debug_buf = nullptr;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
@@ -262,17 +235,12 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   // Tail: the last `split` full tiles are handed out as two half-height tiles each
   // (about one tile per warp; none when the pool is a single wave).
   static const double tail_waves = getenv("IRDN_TAIL") ? atof(getenv("IRDN_TAIL")) : 1.0;
+  // (a short pool only: with many tiles per warp the tail is a small share and the
+  // halves' extra halo rows cost more than they save - c4: 18 tiles/warp, +2 %)
   long long split = wk::WH == 32 ? (long long)(tail_waves * ctas * wk::WARPS) : 0;
-  if (ntiles <= ctas * wk::WARPS) split = 0;
+  if (ntiles <= ctas * wk::WARPS || ntiles >= 8LL * ctas * wk::WARPS) split = 0;
   split = std::min(split, ntiles);
   p.full_tiles = (int)(ntiles - split);
-  static const int ov_keep = getenv("IRDN_OVKEEP") ? atoi(getenv("IRDN_OVKEEP")) : 0;
-  p.ov = method == 0 && ov_keep > 0 ? ov_slot(dev, sched) : nullptr;
-  p.ov_keep = p.ov ? ov_keep : 0;
-  p.ov_cap = kOvCap;
-  p.in = d_in;
-  p.in_pitch = g.in_pitch;
-  p.in_frame = g.in_frame_stride;
   *taken = true;
   cudaError_t e = launch_pdl(wk::fnr_warp_kernel<T, K>, dim3((unsigned)ctas), dim3(wk::THREADS), G::SMEM, s, in_map, p);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -340,7 +308,6 @@ inline int launch_k3_th(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, 
   p.one = 1u;
   p.debug = 0;
   p.full_tiles = 0;
-  p.ov_keep = 0;
   p.debug_buf = nullptr;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;

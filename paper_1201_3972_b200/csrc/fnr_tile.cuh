@@ -81,19 +81,10 @@ struct TileParams {
   int32_t batch;
   int32_t method;     // 0 fnr, 1 mf
   unsigned long long* counts;
-  unsigned int* sched;  // [0] next tile to hand out, [1] finished warps/CTAs, [2]/[3] overflow (reset by the last)
+  unsigned int* sched;  // [0] next tile to hand out, [1] finished warps/CTAs (reset to 0 by the last)
   uint32_t one;         // 1, opaque to the compiler (keeps adds as IMAD on the FMA pipe)
   int32_t debug;        // experiments only: 1 = skip the median stage, 2 = skip the network
   int32_t full_tiles;   // warp kernel: tiles [0, full_tiles) are full height, the rest half-height halves
-  // warp kernel, FNR: a tile with more than ov_keep noisy pixels hands the excess to the
-  // overflow list ov[0, ov_cap) (sched[2] reserved, sched[3] claimed), drained by warps
-  // that find the tile pool empty; ov_keep = 0 disables it.
-  int32_t ov_keep;
-  int32_t ov_cap;
-  unsigned long long* ov;
-  const void* in;       // raw input (same tensor as the map): overflow medians read it directly
-  int64_t in_pitch;
-  int64_t in_frame;
   unsigned long long* debug_buf;  // experiments only (IRDN_TIMELINE builds): per-warp timeline
 };
 

@@ -208,100 +208,6 @@ __device__ __forceinline__ uint32_t medians(const T* s_in, const uint16_t* q, in
   return replaced;
 }
 
-// ---- overflow list (heavy tiles) ---------------------------------------------
-// A warp tile with far more noisy pixels than usual (clusters of hot pixels / sharp
-// texture: up to ~70 % of a tile vs ~8 % typical on c2) takes 5-10x the median time of
-// a normal tile and, picked up late, ends the launch on its own. Such a warp keeps the
-// first ov_keep queue entries and publishes the rest (tile index << 16 | entry, tag bit
-// 63) to a per-launch global list; warps that find the tile pool empty drain the list
-// before they exit, reading the windows straight from the input (in L2).
-//
-// List accounting is one 64-bit word (sched[2..3]: claimed in the low half, reserved in
-// the high half), so a reservation and a claim are each a single atomicAdd and each
-// sees the other's counter exactly:
-//   * claim: atomicAdd(word, 64) -> (rsv, clm); the claimer processes
-//     [clm, min(clm + 64, rsv, cap)). Slots past rsv are "phantom-claimed";
-//   * reserve: atomicAdd(word, g << 32) -> (rsv, clm); slots of [rsv, rsv + g) below
-//     clm were phantom-claimed by a warp that will not process them, and slots at or past
-//     cap do not exist, so the owner publishes only [max(rsv, clm), min(rsv + g, cap))
-//     and keeps the rest in its local queue;
-//   * an owner claims until the list is empty before it exits, so every published entry
-//     is claimed by a running warp; other warps may leave as soon as a read shows the
-//     list empty.
-constexpr unsigned long long kOvTag = 1ull << 63;
-
-__device__ __forceinline__ void ov_publish(unsigned long long* ptr, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(ptr), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ unsigned long long ov_take(unsigned long long* ptr) {
-  unsigned long long v;
-  for (;;) {
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ptr) : "memory");
-    if (v & kOvTag) break;
-    __nanosleep(32);
-  }
-  *ptr = 0ull;  // the list is clean again for the next launch that uses this slot
-  return v;
-}
-
-template <typename T, int K>
-__device__ __forceinline__ uint32_t ov_drain(const tile::TileParams& p, int tiles_per_frame, int lane,
-                                             bool owner) {
-  constexpr int r = K / 2;
-  const T* in = reinterpret_cast<const T*>(p.in);
-  T* out = reinterpret_cast<T*>(p.out);
-  unsigned long long* word = reinterpret_cast<unsigned long long*>(p.sched + 2);
-  uint32_t replaced = 0;
-  for (;;) {
-    unsigned long long w = 0ull;
-    if (lane == 0) {
-      w = *reinterpret_cast<volatile unsigned long long*>(word);
-      const unsigned int rsv0 = (unsigned int)(w >> 32), clm0 = (unsigned int)w;
-      if (owner || clm0 < min(rsv0, (unsigned)p.ov_cap)) w = atomicAdd(word, 64ull);
-    }
-    w = __shfl_sync(0xffffffffu, w, 0);
-    const unsigned int rsv = min((unsigned int)(w >> 32), (unsigned)p.ov_cap), c0 = (unsigned int)w;
-    if (c0 >= rsv) break;
-    const unsigned int take = min(64u, rsv - c0);
-    if ((unsigned)lane < take) {
-      const bool two = (unsigned)lane + 32u < take;
-      const unsigned long long e0 = ov_take(p.ov + c0 + lane);
-      const unsigned long long e1 = two ? ov_take(p.ov + c0 + lane + 32) : e0;
-      int ys[2], xs[2], bs[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const unsigned long long e = h ? e1 : e0;
-        const WTile ti = tile_of(p, (int)((e & ~kOvTag) >> 16), tiles_per_frame);
-        ys[h] = ti.y0 + (int)((e >> 8) & 0xFFu);
-        xs[h] = ti.x0 + (int)(e & 0xFFu);
-        bs[h] = ti.b;
-      }
-      const T* f0 = in + (int64_t)bs[0] * p.in_frame;
-      const T* f1 = in + (int64_t)bs[1] * p.in_frame;
-      uint32_t v[K * K];
-#pragma unroll
-      for (int dy = 0; dy < K; ++dy) {
-        const T* r0 = f0 + (int64_t)(clampi(ys[0] + dy - r, 0, p.height - 1) - p.in_row0) * p.in_pitch;
-        const T* r1 = f1 + (int64_t)(clampi(ys[1] + dy - r, 0, p.height - 1) - p.in_row0) * p.in_pitch;
-#pragma unroll
-        for (int dx = 0; dx < K; ++dx)
-          v[dy * K + dx] = (uint32_t)r0[clampi(xs[0] + dx - r, 0, p.width - 1)] |
-                           ((uint32_t)r1[clampi(xs[1] + dx - r, 0, p.width - 1)] << 16);
-      }
-      const uint32_t c = v[r * K + r];
-      const uint32_t med = tile::median_dispatch<K * K>(v);
-      out[(int64_t)bs[0] * p.out_frame + (int64_t)(ys[0] - p.row_begin) * p.out_pitch + xs[0]] = (T)(med & 0xFFFFu);
-      replaced += (med & 0xFFFFu) != (c & 0xFFFFu);
-      if (two) {
-        out[(int64_t)bs[1] * p.out_frame + (int64_t)(ys[1] - p.row_begin) * p.out_pitch + xs[1]] = (T)(med >> 16);
-        replaced += (med >> 16) != (c >> 16);
-      }
-    }
-  }
-  return replaced;
-}
-
 template <typename T, int K>
 __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant__ CUtensorMap in_map,
                                                            const tile::TileParams p) {
@@ -362,7 +268,6 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
   __syncwarp();
 
   const int c0 = 2 * lane + R;  // smem column of this lane's first pixel
-  bool owner = false;           // this warp published overflow entries (drains until the list is empty)
   T* const out_base = reinterpret_cast<T*>(p.out);
 
 #ifdef IRDN_TIMELINE
@@ -427,65 +332,8 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
       detected += (uint32_t)cnt;
       const int off = incl - cnt;  // index of this lane's first queue entry
       const uint32_t ebase = (uint32_t)(2 * lane);
-      // published entries: queue indices [lo, hi), at list slot ovb + (idx - lo)
-      int lo = 0, hi = 0, ovb = 0;
-      if (n > p.ov_keep && p.ov_keep > 0) {
-        if (lane == 0) {
-          const unsigned long long w0 = *reinterpret_cast<volatile unsigned long long*>(p.sched + 2);
-          const int g = min(n - p.ov_keep, p.ov_cap - (int)min((unsigned)(w0 >> 32), (unsigned)p.ov_cap));
-          if (g > 0) {
-            const unsigned long long w =
-                atomicAdd(reinterpret_cast<unsigned long long*>(p.sched + 2), (unsigned long long)g << 32);
-            const long long rsv = (long long)(w >> 32), clm = (long long)(unsigned int)w;
-            const long long pub0 = max(rsv, clm), pub1 = min(rsv + g, (long long)p.ov_cap);
-            if (pub1 > pub0) {
-              lo = p.ov_keep + (int)(pub0 - rsv);
-              hi = p.ov_keep + (int)(pub1 - rsv);
-              ovb = (int)pub0;
-            }
-          }
-        }
-        lo = __shfl_sync(0xffffffffu, lo, 0);
-        hi = __shfl_sync(0xffffffffu, hi, 0);
-        ovb = __shfl_sync(0xffffffffu, ovb, 0);
-        if (hi > lo) owner = true;
-        if (hi > lo && off + cnt > lo && off < hi) {
-          __threadfence();
-          int idx = off;
-          const unsigned long long tbits = kOvTag | ((unsigned long long)ti.t << 16);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t f = flags[h];
-            while (f) {
-              const int bit = __ffs(f) - 1;
-              f &= f - 1u;
-              if (idx >= lo && idx < hi)
-                ov_publish(p.ov + ovb + (idx - lo),
-                           tbits | (ebase + ((uint32_t)(16 * h + (bit & 15)) << 8) + (uint32_t)(bit >> 4)));
-              ++idx;
-            }
-          }
-        }
-      }
-      const int granted = hi - lo;
-      // local queue: entries [0, lo) and [hi, n), renumbered contiguously
-      const int nl = n - granted;
-      for (int q0 = 0; q0 < nl; q0 += QCAP) {
-        if (granted > 0) {
-          int idx = off;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t f = flags[h];
-            while (f) {
-              const int bit = __ffs(f) - 1;
-              f &= f - 1u;
-              const int li = idx < lo ? idx : idx - granted;
-              if ((idx < lo || idx >= hi) && (unsigned)(li - q0) < (unsigned)QCAP)
-                s_q[li - q0] = (uint16_t)(ebase + ((uint32_t)(16 * h + (bit & 15)) << 8) + (uint32_t)(bit >> 4));
-              ++idx;
-            }
-          }
-        } else if (off < q0 + QCAP && off + cnt > q0) {
+      for (int q0 = 0; q0 < n; q0 += QCAP) {
+        if (off < q0 + QCAP && off + cnt > q0) {
           int idx = off - q0;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -500,7 +348,7 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
           }
         }
         __syncwarp();  // queue visible; centre stores ordered before the median stores
-        replaced += medians<T, K>(s_in, s_q, min(QCAP, nl - q0), out_tile, p.out_pitch, lane, true);
+        replaced += medians<T, K>(s_in, s_q, min(QCAP, n - q0), out_tile, p.out_pitch, lane, true);
         __syncwarp();  // queue reads done before the next round overwrites it
       }
     } else {
@@ -535,26 +383,9 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
     __syncwarp();
     if (lane == 0) refill(stage);
   }
-#ifdef IRDN_TIMELINE
-  uint64_t t_d0, t_d1;
-  IRDN_TL_NOW(t_d0);
-#endif
-  if (fnr && p.ov_keep > 0) replaced += ov_drain<T, K>(p, tiles_per_frame, lane, owner);
-#ifdef IRDN_TIMELINE
-  IRDN_TL_NOW(t_d1);
-  if (lane == 0 && p.debug_buf) {
-    unsigned long long* d = p.debug_buf + 600000 + (size_t)(blockIdx.x * WARPS + warp) * 4;
-    d[0] = t_d0;
-    d[1] = t_d1;
-    d[2] = owner;
-    d[3] = 1;
-  }
-#endif
   if (lane == 0 && atomicAdd(p.sched + 1, 1u) == gridDim.x * WARPS - 1) {
     p.sched[0] = 0u;
     p.sched[1] = 0u;
-    p.sched[2] = 0u;
-    p.sched[3] = 0u;
   }
   if (fnr) block_add_counts<THREADS>(detected, replaced, p.counts);
 }

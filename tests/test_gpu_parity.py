@@ -241,11 +241,10 @@ def test_single_frame_row_pipeline(cuda_ok):
 
 
 @pytest.mark.parametrize("dtype,k", [(np.uint16, 5), (np.uint8, 7), (np.uint16, 11)])
-def test_heavy_tiles_overflow_list(cuda_ok, dtype, k):
-    """Warp tiles with far more noisy pixels than ov_keep hand the excess to the overflow
-    list (fnr_warp.cuh); with the whole batch heavy the list also fills up (kOvCap) and
-    the rest stays with the owning warp. Both must match the oracle bit for bit, whole
-    frames and row strips (input rows offset from the frame)."""
+def test_heavy_tiles(cuda_ok, dtype, k):
+    """Warp tiles with many more noisy pixels than usual (patches, a whole frame, a
+    batch where nearly every pixel is flagged: several queue rounds per tile) match the
+    oracle bit for bit, whole frames and row strips (input rows offset from the frame)."""
     import torch
 
     rng = np.random.default_rng(7)
@@ -256,7 +255,7 @@ def test_heavy_tiles_overflow_list(cuda_ok, dtype, k):
     want, wst = _oracle(img, k, "fnr", 1)
     got, gst = gpu_filter(img, k, "fnr", 1)
     assert np.array_equal(got, want) and gst == wst
-    heavy = rng.integers(0, 4, size=(48, 256, 320)).astype(dtype)  # ~all flagged: list overflows
+    heavy = rng.integers(0, 4, size=(48, 256, 320)).astype(dtype)  # ~all flagged
     want, wst = _oracle(heavy, k, "fnr", 1)
     got, gst = gpu_filter(heavy, k, "fnr", 1)
     assert np.array_equal(got, want) and gst == wst
