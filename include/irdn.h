@@ -14,6 +14,10 @@
  *                                    of a frame whose rows are clamped against the GLOBAL image height
  *   irdn_stats                    <- filters.py:33-52    FilterStats (same field meaning and key order)
  *   IRDN_METHOD_FNR / _MF         <- filters.py:23-24    METHOD_FNR = "fnr", METHOD_MF = "mf"
+ *   irdn_inject_impulse_u8        <- noise.py:89-106     inject_impulse(img, NoiseSpec) (SplitMix64 stream,
+ *                                    noise.py:17-34; bit-identical output image, mask and count)
+ *   irdn_sq_err_sum_u8 / _u16     <- metrics.py:22-32    the exact integer sum inside mse() (and psnr(),
+ *                                    quality_report(), build_comparison())
  *
  * Semantics (bit-exact with the reference):
  *   - row-major frames, origin top-left; replicate-edge (clamp) window gather;
@@ -138,6 +142,30 @@ IRDN_API int irdn_run_filter_device_u16(const uint16_t* d_in, uint16_t* d_out, u
                                int64_t batch, int64_t height, int64_t width, int32_t k,
                                int32_t method, int32_t passes, unsigned long long* d_counts,
                                void* stream);
+
+/*
+ * inject_impulse (noise.py:89-106) over n row-major u8 pixels, device buffers,
+ * stream-ordered. Draw p of SplitMix64(seed) (noise.py:17-34) is mix(seed +
+ * (p+1) * 0x9E3779B97F4A7C15); per pixel one uniform (top 53 bits / 2^53) < density
+ * decides corruption and, only then, a second one < salt_fraction picks 255 over 0.
+ * d_out receives the noisy image (d_out != d_in), d_flags (optional, may be NULL)
+ * the NoiseMask flags (1 = corrupted), *d_count (optional) is INCREMENTED by the
+ * number of corrupted pixels. density / salt_fraction outside [0, 1] -> IRDN_EINVAL
+ * (NoiseSpec.__post_init__, noise.py:45-55). Uses ~n/4 bytes of stream-ordered
+ * scratch (cudaMallocAsync).
+ */
+IRDN_API int irdn_inject_impulse_u8(const uint8_t* d_in, uint8_t* d_out, uint8_t* d_flags, int64_t n,
+                                    uint64_t seed, double density, double salt_fraction,
+                                    unsigned long long* d_count, void* stream);
+
+/*
+ * Exact sum over i of (a[i] - b[i])^2 (metrics.py:29-32), ADDED to *d_sum, device
+ * buffers, stream-ordered. u16: n <= 2^32 - 1 per call (the sum must fit 64 bits).
+ */
+IRDN_API int irdn_sq_err_sum_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t n,
+                                unsigned long long* d_sum, void* stream);
+IRDN_API int irdn_sq_err_sum_u16(const uint16_t* d_a, const uint16_t* d_b, int64_t n,
+                                 unsigned long long* d_sum, void* stream);
 
 /* Kernel launches issued by this thread since the last reset (for bench accounting). */
 IRDN_API uint64_t irdn_launch_count(void);

@@ -316,3 +316,48 @@ int oracle_run_filter(const void* px, int bpp, int64_t batch, int64_t w, int64_t
   stats->elapsed_ms = (double)(t1.tv_sec - t0.tv_sec) * 1e3 + (double)(t1.tv_nsec - t0.tv_nsec) * 1e-6;
   return 0;
 }
+
+/* ---- inject_impulse (noise.py:89-106) ----------------------------------------
+ * SplitMix64.next_u64 (noise.py:25-30): state += 0x9E3779B97F4A7C15, then the two
+ * xor-shift-multiply rounds and a final xor-shift; next_uniform (noise.py:32-34) is
+ * (next_u64 >> 11) / 2^53 as a double. Pixels in row-major order: one uniform draw
+ * decides corruption (< density); only a corrupted pixel draws again (< salt_fraction
+ * -> 255, else 0). Restated sequentially, exactly as the reference walks it. */
+static uint64_t splitmix_next(uint64_t* state) {
+  *state += 0x9E3779B97F4A7C15ull;
+  uint64_t z = *state;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static double splitmix_uniform(uint64_t* state) {
+  return (double)(splitmix_next(state) >> 11) / 9007199254740992.0;
+}
+
+uint64_t oracle_inject_impulse(const uint8_t* in, uint8_t* out, uint8_t* flags, int64_t n,
+                               uint64_t seed, double density, double salt_fraction) {
+  uint64_t state = seed, count = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    uint8_t v = in[i], f = 0;
+    if (splitmix_uniform(&state) < density) {
+      v = splitmix_uniform(&state) < salt_fraction ? 255 : 0;
+      f = 1;
+      ++count;
+    }
+    out[i] = v;
+    if (flags) flags[i] = f;
+  }
+  return count;
+}
+
+/* ---- mse numerator (metrics.py:29-32) ---------------------------------------- */
+uint64_t oracle_sq_err_sum(const void* a, const void* b, int bpp, int64_t n) {
+  uint64_t total = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t pa = bpp == 1 ? ((const uint8_t*)a)[i] : ((const uint16_t*)a)[i];
+    const int64_t pb = bpp == 1 ? ((const uint8_t*)b)[i] : ((const uint16_t*)b)[i];
+    total += (uint64_t)((pa - pb) * (pa - pb));
+  }
+  return total;
+}

@@ -37,4 +37,10 @@ int oracle_run_pass(const void* px, int bpp, int64_t batch, int64_t w, int64_t h
                     int threads, void* out, oracle_stats* stats);
 int oracle_run_filter(const void* px, int bpp, int64_t batch, int64_t w, int64_t h, int k,
                       int method, int passes, int threads, void* out, oracle_stats* stats);
+/* noise.py:89-106 inject_impulse on n u8 pixels, sequential SplitMix64 (noise.py:17-34);
+ * returns the number of corrupted pixels. */
+uint64_t oracle_inject_impulse(const uint8_t* in, uint8_t* out, uint8_t* flags, int64_t n,
+                               uint64_t seed, double density, double salt_fraction);
+/* metrics.py:29-32: exact sum of squared differences (bpp 1 or 2). */
+uint64_t oracle_sq_err_sum(const void* a, const void* b, int bpp, int64_t n);
 #endif

@@ -82,6 +82,11 @@ def lib() -> ctypes.CDLL:
         l.oracle_median_of.restype = ctypes.c_int
         l.oracle_sort_values.argtypes = [vp, ctypes.c_int, ctypes.POINTER(_SortCounters)]
         l.oracle_sort_values.restype = ctypes.c_int
+        l.oracle_inject_impulse.argtypes = [vp, vp, vp, i64, ctypes.c_uint64, ctypes.c_double,
+                                            ctypes.c_double]
+        l.oracle_inject_impulse.restype = ctypes.c_uint64
+        l.oracle_sq_err_sum.argtypes = [vp, vp, ctypes.c_int, i64]
+        l.oracle_sq_err_sum.restype = ctypes.c_uint64
         _lib = l
     return _lib
 
@@ -187,3 +192,21 @@ def run_filter_np(img: np.ndarray, k: int, method: str = "fnr", passes: int = 1)
         cur = out
     res = cur if img.ndim == 3 else cur[0]
     return res, Stats(scans, sorts, repl, det, passes)
+
+
+def inject_impulse_c(pixels: np.ndarray, seed: int, density: float, salt_fraction: float = 0.5):
+    """noise.py:89-106 restated in C: returns (noisy u8 array, flags u8 array, count)."""
+    a = np.ascontiguousarray(pixels, dtype=np.uint8)
+    out = np.empty_like(a)
+    flags = np.empty_like(a)
+    cnt = lib().oracle_inject_impulse(a.ctypes.data, out.ctypes.data, flags.ctypes.data, a.size,
+                                      seed & 0xFFFFFFFFFFFFFFFF, density, salt_fraction)
+    return out, flags, int(cnt)
+
+
+def sq_err_sum_c(a: np.ndarray, b: np.ndarray) -> int:
+    """metrics.py:29-32 numerator (exact)."""
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    assert a.dtype == b.dtype and a.size == b.size
+    return int(lib().oracle_sq_err_sum(a.ctypes.data, b.ctypes.data, a.dtype.itemsize, a.size))

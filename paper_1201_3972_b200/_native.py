@@ -47,7 +47,7 @@ EXPORTED = [
     "irdn_filter_pass_u8", "irdn_filter_pass_u16", "irdn_filter_strip_u8", "irdn_filter_strip_u16",
     "irdn_run_filter_u8", "irdn_run_filter_u16", "irdn_run_filter_device_u8",
     "irdn_run_filter_device_u16", "irdn_launch_count", "irdn_reset_launch_count",
-    "irdn_set_force_generic",
+    "irdn_set_force_generic", "irdn_inject_impulse_u8", "irdn_sq_err_sum_u8", "irdn_sq_err_sum_u16",
 ]
 
 
@@ -80,6 +80,13 @@ def _declare(l: ctypes.CDLL) -> None:
     l.irdn_reset_launch_count.argtypes = []
     l.irdn_set_force_generic.restype = i32
     l.irdn_set_force_generic.argtypes = [i32]
+    l.irdn_inject_impulse_u8.restype = ctypes.c_int
+    l.irdn_inject_impulse_u8.argtypes = [vp, vp, vp, i64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+                                         vp, vp]
+    for t in ("u8", "u16"):
+        f = getattr(l, f"irdn_sq_err_sum_{t}")
+        f.restype = ctypes.c_int
+        f.argtypes = [vp, vp, i64, vp, vp]
 
 
 def load_lib() -> ctypes.CDLL:

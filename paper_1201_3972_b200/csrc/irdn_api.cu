@@ -9,6 +9,7 @@
 // launches sm_100a kernels or fails with IRDN_ENODEV / IRDN_ECUDA.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -21,6 +22,8 @@
 #include "fnr_common.cuh"
 #include "fnr_generic.cuh"
 #include "fnr_fast.cuh"
+#include "metrics.cuh"
+#include "noise.cuh"
 
 namespace irdn {
 
@@ -350,6 +353,83 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   return IRDN_OK;
 }
 
+// ---- inject_impulse (noise.py:89-106), csrc/noise.cuh ------------------------
+static int inject_impulse(const uint8_t* d_in, uint8_t* d_out, uint8_t* d_flags, int64_t n, uint64_t seed,
+                          double density, double salt, unsigned long long* d_count, void* stream) {
+  if (!(density >= 0.0 && density <= 1.0))  // noise.py:47-48
+    return fail(IRDN_EINVAL, "density must be in [0, 1], got %g", density);
+  if (!(salt >= 0.0 && salt <= 1.0))  // noise.py:49-52
+    return fail(IRDN_EINVAL, "salt_fraction must be in [0, 1], got %g", salt);
+  if (n < 0) return fail(IRDN_EINVAL, "pixel count must be >= 0, got %lld", (long long)n);
+  if (n > ((int64_t)1 << 40)) return fail(IRDN_EINVAL, "too many pixels (%lld)", (long long)n);
+  if (n > 0 && (!d_in || !d_out)) return fail(IRDN_EINVAL, "null image pointer");
+  if (n > 0 && d_in == d_out) return fail(IRDN_EINVAL, "in-place injection is not supported (d_out == d_in)");
+  int rc = check_device(nullptr);
+  if (rc != IRDN_OK) return rc;
+  if (n == 0) return IRDN_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  noise::Params p;
+  p.in = d_in;
+  p.out = d_out;
+  p.flags = d_flags;
+  p.count = d_count;
+  p.n = n;
+  p.nwords = (2 * n + noise::WORD - 1) / noise::WORD;
+  p.nchunks = (p.nwords + noise::THREADS - 1) / noise::THREADS;
+  p.seed = seed;
+  // (x >> 11) / 2^53 < d  <=>  (x >> 11) < ceil(d * 2^53): d * 2^53 is exact in binary64
+  p.thr_density = (uint64_t)std::ceil(std::ldexp(density, 53));
+  p.thr_salt = (uint64_t)std::ceil(std::ldexp(salt, 53));
+  const size_t words_b = (size_t)p.nwords * sizeof(uint32_t);
+  const size_t chunks_b = (size_t)p.nchunks * (sizeof(noise::Fn) + sizeof(uint2) + sizeof(unsigned long long));
+  void* ws = nullptr;
+  IRDN_CUDA(cudaMallocAsync(&ws, 2 * words_b + chunks_b + 64, s));
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  p.cbits = reinterpret_cast<uint32_t*>(w8);
+  p.sbits = reinterpret_cast<uint32_t*>(w8 + words_b);
+  size_t off = (2 * words_b + 15) & ~(size_t)15;
+  p.chunk_fn = reinterpret_cast<noise::Fn*>(w8 + off);
+  off += (size_t)p.nchunks * sizeof(noise::Fn);
+  p.chunk_off = reinterpret_cast<unsigned long long*>(w8 + off);
+  off += (size_t)p.nchunks * sizeof(unsigned long long);
+  p.chunk_entry = reinterpret_cast<uint2*>(w8 + off);
+  const dim3 grid((unsigned)p.nchunks);
+  noise::noise_draws_kernel<<<grid, noise::THREADS, 0, s>>>(p);
+  noise::noise_chunks_kernel<<<1, noise::THREADS, 0, s>>>(p);
+  noise::noise_emit_kernel<<<grid, noise::THREADS, 0, s>>>(p);
+  g_launches += 3;
+  cudaError_t e = cudaGetLastError();
+  cudaError_t e2 = cudaFreeAsync(ws, s);
+  if (e != cudaSuccess) return fail(IRDN_ECUDA, "inject_impulse launch failed: %s", cudaGetErrorString(e));
+  if (e2 != cudaSuccess) return fail(IRDN_ECUDA, "cudaFreeAsync failed: %s", cudaGetErrorString(e2));
+  return IRDN_OK;
+}
+
+// ---- exact squared-error sum (metrics.py:22-32), csrc/metrics.cuh -------------
+template <typename T>
+static int sq_err_sum(const T* d_a, const T* d_b, int64_t n, unsigned long long* d_sum, void* stream) {
+  if (n < 0) return fail(IRDN_EINVAL, "element count must be >= 0, got %lld", (long long)n);
+  if (sizeof(T) == 2 && n > (int64_t)0xFFFFFFFFLL)
+    return fail(IRDN_EINVAL, "u16 squared-error sum takes at most 2^32-1 elements per call, got %lld",
+                (long long)n);
+  if (!d_sum || (n > 0 && (!d_a || !d_b))) return fail(IRDN_EINVAL, "null pointer");
+  int dev = 0;
+  int rc = check_device(&dev);
+  if (rc != IRDN_OK) return rc;
+  if (n == 0) return IRDN_OK;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool vec = ((reinterpret_cast<uintptr_t>(d_a) | reinterpret_cast<uintptr_t>(d_b)) & 15) == 0;
+  const int64_t per_cta = (int64_t)metrics::THREADS * 16 / (int64_t)sizeof(T) * 4;
+  const int64_t want = (n + per_cta - 1) / per_cta;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+  metrics::sq_err_kernel<T><<<grid, metrics::THREADS, 0, static_cast<cudaStream_t>(stream)>>>(d_a, d_b, n, vec,
+                                                                                                d_sum);
+  ++g_launches;
+  IRDN_CUDA(cudaGetLastError());
+  return IRDN_OK;
+}
+
 }  // namespace irdn
 
 using namespace irdn;
@@ -425,6 +505,18 @@ int irdn_run_filter_device_u16(const uint16_t* d_in, uint16_t* d_out, uint16_t* 
                                void* stream) {
   return run_device<uint16_t>(d_in, d_out, d_tmp, batch, height, width, k, method, passes,
                               d_counts, stream);
+}
+int irdn_inject_impulse_u8(const uint8_t* d_in, uint8_t* d_out, uint8_t* d_flags, int64_t n, uint64_t seed,
+                           double density, double salt_fraction, unsigned long long* d_count, void* stream) {
+  return inject_impulse(d_in, d_out, d_flags, n, seed, density, salt_fraction, d_count, stream);
+}
+int irdn_sq_err_sum_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t n, unsigned long long* d_sum,
+                       void* stream) {
+  return sq_err_sum<uint8_t>(d_a, d_b, n, d_sum, stream);
+}
+int irdn_sq_err_sum_u16(const uint16_t* d_a, const uint16_t* d_b, int64_t n, unsigned long long* d_sum,
+                        void* stream) {
+  return sq_err_sum<uint16_t>(d_a, d_b, n, d_sum, stream);
 }
 uint64_t irdn_launch_count(void) { return g_launches; }
 void irdn_reset_launch_count(void) { g_launches = 0; }

@@ -17,6 +17,12 @@ Files:
   ref_fixtures.npz   structured_image + inject_impulse (Appendix A), ramp 364x244, ramp16
   ref_sort.npz       sort_values / median_of on random multisets and m3killer permutations
   ref_configs.npz    crops of the five BASELINE config scenes through the reference
+  ref_noise.npz      inject_impulse (noise.py:89-106): noisy image, mask flags, count
+  ref_metrics.npz    mse / psnr / quality_report / build_comparison (metrics.py) on image pairs
+  ref_pgm.json       load_pgm on well-formed and malformed P5/P2 bytes (result sha or PgmError text),
+                     save_pgm bytes, fixture (ramp/radial/structured) shas
+
+    python tests/golden/make_golden.py noise metrics   # only the named sets
 """
 
 from __future__ import annotations
@@ -263,14 +269,152 @@ def make_configs():
     s.save("ref_configs.npz")
 
 
+def make_noise():
+    rng = np.random.default_rng(424242)
+    arrays, meta = {}, []
+    clean = R.structured_image()
+    cases = [(clean, 0.2, 0.5, 42), (clean, 0.3, 0.5, 42), (clean, 0.0, 0.5, 42), (clean, 1.0, 0.5, 7),
+             (clean, 1.0, 0.0, 7), (clean, 1.0, 1.0, 7), (clean, 0.5, 0.25, 0),
+             (clean, 0.5, 0.75, 2**64 - 1), (clean, 0.05, 0.5, 123456789), (clean, 0.999, 0.001, 99)]
+    for h, w in ((1, 1), (1, 37), (33, 65), (257, 129), (64, 1000)):
+        img = R.GrayImage(w, h, rng.integers(0, 256, h * w, dtype=np.uint8).tobytes())
+        cases.append((img, float(rng.choice([0.1, 0.3, 0.6])), 0.5, int(rng.integers(0, 2**63))))
+    for i, (img, d, salt, seed) in enumerate(cases):
+        noisy, mask = R.inject_impulse(img, R.NoiseSpec(d, salt, seed))
+        a = np.frombuffer(bytes(img.pixels), np.uint8).reshape(img.height, img.width).copy()
+        arrays[f"in{i}"] = a
+        arrays[f"out{i}"] = np.frombuffer(bytes(noisy.pixels), np.uint8).reshape(a.shape).copy()
+        arrays[f"flags{i}"] = np.frombuffer(bytes(mask.flags), np.uint8).reshape(a.shape).copy()
+        meta.append(dict(density=d, salt_fraction=salt, seed=seed, count=mask.count,
+                         sha=sha16(arrays[f"out{i}"])))
+        print(f"noise {a.shape} d={d} salt={salt} seed={seed}: count {mask.count} sha {meta[-1]['sha']}")
+    np.savez_compressed(os.path.join(HERE, "ref_noise.npz"), meta=np.array(json.dumps(meta)), **arrays)
+    print(f"wrote ref_noise.npz: {len(meta)} cases")
+
+
+def make_metrics():
+    from irdenoise import metrics as M
+
+    rng = np.random.default_rng(777)
+    arrays, meta = {}, []
+    clean = R.structured_image()
+    pairs = [(clean, clean)]
+    noisy, _ = R.inject_impulse(clean, R.NoiseSpec(0.2, 0.5, 42))
+    pairs.append((clean, noisy))
+    for h, w in ((1, 1), (3, 5), (64, 97)):
+        a = R.GrayImage(w, h, rng.integers(0, 256, h * w, dtype=np.uint8).tobytes())
+        b = R.GrayImage(w, h, rng.integers(0, 256, h * w, dtype=np.uint8).tobytes())
+        pairs.append((a, b))
+    a = R.GrayImage(40, 30, bytes([0]) * 1200)
+    b = R.GrayImage(40, 30, bytes([255]) * 1200)
+    pairs.append((a, b))
+    for i, (a, b) in enumerate(pairs):
+        arrays[f"a{i}"] = np.frombuffer(bytes(a.pixels), np.uint8).reshape(a.height, a.width).copy()
+        arrays[f"b{i}"] = np.frombuffer(bytes(b.pixels), np.uint8).reshape(b.height, b.width).copy()
+        q = M.quality_report(a, b)
+        q100 = M.quality_report(a, b, max_val=100)
+        meta.append(dict(mse=M.mse(a, b).hex(), psnr=repr(M.psnr(a, b)), psnr100=repr(M.psnr(a, b, 100)),
+                         report=[q.mse.hex(), repr(q.psnr_db), q.max_val],
+                         report100=[q100.mse.hex(), repr(q100.psnr_db), q100.max_val],
+                         format_db=M.format_db(M.psnr(a, b))))
+    # one full comparison row (cli.py:132-150) with the reference filters; elapsed_ms dropped
+    rows = []
+    for d in (0.2, 0.3):
+        noisy, _ = R.inject_impulse(clean, R.NoiseSpec(d, 0.5, 42))
+        spec = R.WindowSpec(3)
+        mf_out, mf_st = R.run_filter(noisy, spec, "mf", 2)
+        fnr_out, fnr_st = R.run_filter(noisy, spec, "fnr", 2)
+        row = M.build_comparison(clean, noisy, mf_out, mf_st, fnr_out, fnr_st, d).to_dict()
+        for m in row["methods"].values():
+            m.pop("elapsed_ms")
+        rows.append(row)
+    np.savez_compressed(os.path.join(HERE, "ref_metrics.npz"),
+                        meta=np.array(json.dumps({"pairs": meta, "rows": rows})), **arrays)
+    print(f"wrote ref_metrics.npz: {len(meta)} pairs, {len(rows)} comparison rows")
+
+
+def make_pgm():
+    import base64
+
+    from irdenoise import fixtures as FX
+    from irdenoise import image as IM
+
+    cases = [
+        b"P5\n3 2\n255\n\x00\x01\x02\x03\x04\x05",
+        b"P5 3 2 255 \x00\x01\x02\x03\x04\x05extra",
+        b"P5\n# comment\n3 # mid\n2\n255\n\x00\x01\x02\x03\x04\x05",
+        b"P5\n3 2\n255\r\x00\x01\x02\x03\x04\x05",
+        b"P5\n3 2\n255\n\x00\x01\x02\x03\x04",
+        b"P5\n3 2\n100\n\x00\x01\x02\x03\x04\x65",
+        b"P5\n3 2\n100\n\x00\x01\x02\x03\x04\x64",
+        b"P5\n3 2\n255",
+        b"P5\n3 2\n256\n\x00\x01\x02\x03\x04\x05",
+        b"P5\n3 2\n0\n\x00\x01\x02\x03\x04\x05",
+        b"P5\n0 2\n255\n",
+        b"P5\n-3 2\n255\n\x00",
+        b"P5\nx 2\n255\n\x00",
+        b"P5\n3",
+        b"P5\n3 2\n",
+        b"P6\n3 2\n255\n\x00\x01\x02\x03\x04\x05\x00\x01\x02\x03\x04\x05",
+        b"P",
+        b"",
+        b"P2\n3 2\n255\n0 1 2\n3 4 5\n",
+        b"P2\n3 2\n255\n0 1 2\n# c\n3 4 5",
+        b"P2\n3 2\n255\n0 1 2 3 4",
+        b"P2\n3 2\n255\n0 1 2 3 4 x",
+        b"P2\n3 2\n7\n0 1 2 3 4 8",
+        b"P2\n3 2\n255\n0 1 2 3 4 256",
+        b"P2\n3 2\n255\n+0 1 2 3 4 5",
+        b"P2\n3 2\n255\n0 1 2 3 4 5 6 7",
+        b"P2\n3 2\n255\n0#c\n1 2 3 4 5",
+        b"P2 2 2 15 1 2 3 4",
+        b"P2\n1 1\n255\n-0",
+        b"P5\n2 2\n255 \x00\x01\x02\x03",
+        b"P5\n2 2\n255\x00\x01\x02\x03\x04",
+        b"P5\t2\t2\t255\t\x00\x01\x02\x03",
+    ]
+    rng = np.random.default_rng(99)
+    big = rng.integers(0, 256, (40, 50), dtype=np.uint8)
+    cases.append(b"P5\n50 40\n255\n" + big.tobytes())
+    cases.append(b"P2\n50 40\n255\n" + b"\n".join(b" ".join(str(v).encode() for v in row) for row in big))
+    out = []
+    for data in cases:
+        try:
+            img = IM.load_pgm(data)
+            res = {"ok": [img.width, img.height, hashlib.sha256(bytes(img.pixels)).hexdigest()],
+                   "saved": hashlib.sha256(IM.save_pgm(img)).hexdigest()}
+        except IM.PgmError as e:
+            res = {"error": str(e)}
+        out.append({"data": base64.b64encode(data).decode(), **res})
+    fx = {}
+    for name in FX.FIXTURE_NAMES:
+        for w, h in ((128, 128), (1, 1), (7, 5), (364, 244), (2, 9)):
+            try:
+                img = FX.make_fixture(name, w, h)
+                fx[f"{name}_{w}x{h}"] = hashlib.sha256(bytes(img.pixels)).hexdigest()
+            except ValueError as e:
+                fx[f"{name}_{w}x{h}"] = "error: " + str(e)
+    with open(os.path.join(HERE, "ref_pgm.json"), "w") as fh:
+        json.dump({"load": out, "fixtures": fx}, fh, indent=0)
+    print(f"wrote ref_pgm.json: {len(out)} codec cases, {len(fx)} fixtures")
+
+
 def main():
+    only = set(sys.argv[1:])
     rng = np.random.default_rng(20260119)
     random.seed(1)
-    make_sort(rng)
-    make_fixtures()
-    make_u8(rng)
-    make_u16(rng)
-    make_configs()
+    if not only:
+        make_sort(rng)
+        make_fixtures()
+        make_u8(rng)
+        make_u16(rng)
+        make_configs()
+    if not only or "noise" in only:
+        make_noise()
+    if not only or "metrics" in only:
+        make_metrics()
+    if not only or "pgm" in only:
+        make_pgm()
 
 
 if __name__ == "__main__":
