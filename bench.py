@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--path", default="filter", choices=["filter", "noise", "sqerr"],
+                    help="filter (default, the BASELINE metric) or a widened row (bench_aux.py)")
     return ap.parse_args()
 
 
@@ -485,6 +487,10 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
 
 def main():
     args = parse()
+    if args.path != "filter":
+        import bench_aux
+
+        return {"noise": bench_aux.run_noise, "sqerr": bench_aux.run_sqerr}[args.path](args, sys.modules[__name__])
     from paper_1201_3972_b200.scene import CONFIGS
 
     cfg = CONFIGS[args.config]

@@ -368,36 +368,43 @@ static int inject_impulse(const uint8_t* d_in, uint8_t* d_out, uint8_t* d_flags,
   if (rc != IRDN_OK) return rc;
   if (n == 0) return IRDN_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   noise::Params p;
   p.in = d_in;
   p.out = d_out;
   p.flags = d_flags;
   p.count = d_count;
   p.n = n;
-  p.nwords = (2 * n + noise::WORD - 1) / noise::WORD;
-  p.nchunks = (p.nwords + noise::THREADS - 1) / noise::THREADS;
+  p.max_chunks = (2 * n + noise::CHUNK - 1) / noise::CHUNK;
   p.seed = seed;
   // (x >> 11) / 2^53 < d  <=>  (x >> 11) < ceil(d * 2^53): d * 2^53 is exact in binary64
-  p.thr_density = (uint64_t)std::ceil(std::ldexp(density, 53));
-  p.thr_salt = (uint64_t)std::ceil(std::ldexp(salt, 53));
-  const size_t words_b = (size_t)p.nwords * sizeof(uint32_t);
-  const size_t chunks_b = (size_t)p.nchunks * (sizeof(noise::Fn) + sizeof(uint2) + sizeof(unsigned long long));
+  const uint64_t thr_density = (uint64_t)std::ceil(std::ldexp(density, 53));
+  const uint64_t thr_salt = (uint64_t)std::ceil(std::ldexp(salt, 53));
+  p.all_density = thr_density >= (1ull << 53);
+  p.all_salt = thr_salt >= (1ull << 53);
+  p.z_density = p.all_density ? 0ull : thr_density << 11;
+  p.z_salt = p.all_salt ? 0ull : thr_salt << 11;
+  p.vec = ((reinterpret_cast<uintptr_t>(d_in) | reinterpret_cast<uintptr_t>(d_out) |
+            reinterpret_cast<uintptr_t>(d_flags)) & 15) == 0;
+  const size_t ws_bytes = 16 + (size_t)p.max_chunks * sizeof(unsigned long long);
   void* ws = nullptr;
-  IRDN_CUDA(cudaMallocAsync(&ws, 2 * words_b + chunks_b + 64, s));
-  uint8_t* w8 = static_cast<uint8_t*>(ws);
-  p.cbits = reinterpret_cast<uint32_t*>(w8);
-  p.sbits = reinterpret_cast<uint32_t*>(w8 + words_b);
-  size_t off = (2 * words_b + 15) & ~(size_t)15;
-  p.chunk_fn = reinterpret_cast<noise::Fn*>(w8 + off);
-  off += (size_t)p.nchunks * sizeof(noise::Fn);
-  p.chunk_off = reinterpret_cast<unsigned long long*>(w8 + off);
-  off += (size_t)p.nchunks * sizeof(unsigned long long);
-  p.chunk_entry = reinterpret_cast<uint2*>(w8 + off);
-  const dim3 grid((unsigned)p.nchunks);
-  noise::noise_draws_kernel<<<grid, noise::THREADS, 0, s>>>(p);
-  noise::noise_chunks_kernel<<<1, noise::THREADS, 0, s>>>(p);
-  noise::noise_emit_kernel<<<grid, noise::THREADS, 0, s>>>(p);
-  g_launches += 3;
+  IRDN_CUDA(cudaMallocAsync(&ws, ws_bytes, s));
+  IRDN_CUDA(cudaMemsetAsync(ws, 0, ws_bytes, s));
+  p.ctl = static_cast<unsigned int*>(ws);
+  p.status = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(ws) + 16);
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, noise::noise_kernel, noise::THREADS, 0) !=
+            cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+  }
+  const long long grid = std::min<long long>(p.max_chunks, (long long)sms * per_sm);
+  noise::noise_kernel<<<(unsigned)grid, noise::THREADS, 0, s>>>(p);
+  ++g_launches;
   cudaError_t e = cudaGetLastError();
   cudaError_t e2 = cudaFreeAsync(ws, s);
   if (e != cudaSuccess) return fail(IRDN_ECUDA, "inject_impulse launch failed: %s", cudaGetErrorString(e));
