@@ -1,0 +1,58 @@
+"""bench.py output contract (the driver parses its last stdout line as JSON).
+
+CPU: the reference arm (`--impl reference`, the oracle port on host cores).
+GPU: the B200 arm (default filter path, `--passes 2`, the widened rows `--path`).
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import REPO
+
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config"}
+
+
+def _run(args, timeout=900):
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), *args], capture_output=True, text=True,
+                         timeout=timeout, cwd=REPO)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = out.stdout.strip().splitlines()[-1]
+    return json.loads(line)
+
+
+def test_reference_arm_line():
+    d = _run(["--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "1"])
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "Mpix/s"
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["config"]["workload"].startswith("c1")
+
+
+@pytest.mark.gpu
+def test_b200_arm_line(cuda_ok):
+    d = _run(["--steps", "50", "--warmup", "3", "--cpu-seconds", "1"])
+    assert BASE_KEYS <= set(d) and "impl" not in d
+    assert d["config"]["workload"].startswith("c2") and d["dtype"] == "u16"
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= 50
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+def test_b200_arm_passes2_and_widened_rows(cuda_ok):
+    d = _run(["--steps", "20", "--warmup", "3", "--passes", "2", "--no-cpu-baseline"])
+    assert d["config"]["passes"] == 2 and d["gpu_launches"] >= 40
+    for path in ("noise", "sqerr"):
+        d = _run(["--path", path, "--steps", "10", "--warmup", "3", "--cpu-seconds", "1"])
+        assert BASE_KEYS <= set(d) and d["value"] > 0 and d["roofline"]["unit"] == "GB/s"
+        assert d["cpu_baseline"]["value"] > 0 and d["e2e"]["value"] > 0
