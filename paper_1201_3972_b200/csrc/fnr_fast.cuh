@@ -328,6 +328,9 @@ inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int
                      unsigned long long* counts, cudaStream_t s, bool* taken) {
   const long long tiles128 = (long long)((g.width + k3::TW - 1) / k3::TW) *
                              ((g.row_end - g.row_begin + 127) / 128) * g.batch;
+  const long long tiles32 = (long long)((g.width + k3::TW - 1) / k3::TW) * ((g.row_end - g.row_begin + 31) / 32) *
+                            g.batch;
+  if (tiles32 < 148) return launch_k3_th<16>(d_in, d_out, g, method, counts, s, taken);  // c1: 128 tiles
   if (tiles128 < 2 * 148) return launch_k3_th<32>(d_in, d_out, g, method, counts, s, taken);
   return launch_k3_th<128>(d_in, d_out, g, method, counts, s, taken);
 }

@@ -33,7 +33,8 @@ constexpr int TPR = TW / COLS;          // threads per row band (16)
 constexpr int BANDS = THREADS / TPR;    // row bands per tile (8)
 constexpr int NSTAGE = 2;
 // Tile height: 128 rows (16 per thread) for large frames, 32 rows (4 per thread) when a
-// frame has too few 128-row tiles to fill the GPU (BASELINE c1: 512x512).
+// frame has too few 128-row tiles to fill the GPU, 16 rows (2 per thread) when even
+// 32-row tiles leave SMs idle (BASELINE c1: 512x512 -> 128 tiles).
 
 template <int TH>
 struct Geo {
