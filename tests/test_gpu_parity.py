@@ -268,3 +268,72 @@ def test_heavy_tiles(cuda_ok, dtype, k):
         det += d
     assert torch.equal(as_i32(torch.cat(parts)), as_i32(whole)) and det == st.detected
     assert np.array_equal(as_i32(whole).cpu().numpy().astype(dtype), _oracle(img[10], k)[0])
+
+
+def test_concurrent_calls_from_threads_and_streams(cuda_ok):
+    """The C ABI is reentrant: host-buffer calls from several threads (per-device workspace
+    lock) and device calls on separate streams (one scheduler slot per launch) in flight
+    together give the single-call results."""
+    import threading
+
+    import torch
+
+    cfg = CONFIGS["c2"].with_shape(height=256, width=320)
+    imgs = [generate(cfg, frame0=4 * i, nframes=4) for i in range(6)]
+    want = [_oracle(im, 5, "fnr", 2) for im in imgs]
+    got = [None] * len(imgs)
+    errs = []
+
+    def host_worker(i):
+        try:
+            got[i] = gpu_filter(imgs[i], 5, "fnr", 2)
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    def device_worker(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                t = torch.from_numpy(imgs[i].view(np.int16)).cuda(non_blocking=False).view(torch.uint16)
+                out, st = P.run_filter(t, P.WindowSpec(5), "fnr", 2)
+                s.synchronize()
+                got[i] = (as_i32(out).cpu().numpy().astype(np.uint16), counters(st))
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    threads = [threading.Thread(target=host_worker if i % 2 == 0 else device_worker, args=(i,))
+               for i in range(len(imgs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errs, errs
+    for (w, wst), (g, gst) in zip(want, got):
+        assert np.array_equal(g, w) and gst == wst
+
+
+def test_cta_tile_kernel_family_matches_oracle(cuda_ok, tmp_path):
+    """IRDN_KERNEL=tile selects the CTA-tile kernel (csrc/fnr_tile.cuh) kept for comparison;
+    it must stay bit-exact too (run in a subprocess: the selection is read once)."""
+    import subprocess
+    import sys
+
+    script = tmp_path / "tile_check.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {str(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))!r})\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.abspath(__file__))!r})\n"
+        "import paper_1201_3972_b200 as P\n"
+        "from oracle import oracle\n"
+        "from paper_1201_3972_b200.scene import CONFIGS, generate\n"
+        "for name, k in (('c2', 5), ('c3', 7), ('c4', 11)):\n"
+        "    cfg = CONFIGS[name].with_shape(height=300, width=400)\n"
+        "    img = generate(cfg, nframes=2)\n"
+        "    got, st = P.run_filter(img, P.WindowSpec(k), 'fnr', 1)\n"
+        "    want, wst = oracle.run_filter_c(img, k, 'fnr', 1, threads=8)\n"
+        "    assert np.array_equal(got, want), name\n"
+        "    assert [st.minmax_scans, st.sorts, st.replacements, st.detected, st.passes] == list(wst.counters())\n"
+        "print('tile ok')\n")
+    env = dict(os.environ, IRDN_KERNEL="tile")
+    out = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0 and "tile ok" in out.stdout, out.stderr[-2000:]
