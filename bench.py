@@ -101,6 +101,22 @@ def read_profile_traffic(cfg_name: str):
         return None, {}
 
 
+def read_alu_floor(cfg_name: str):
+    """ALU-pipe lane-ops per pixel of the dominant kernel (tools/prof/alu_floor.py output)."""
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(REPO, "profiles", "alu_floor_*.json")))
+    for path in reversed(paths):  # newest capture tag first
+        try:
+            for row in json.load(open(path)):
+                if row["config"] == cfg_name:
+                    return dict(row, source=os.path.relpath(path, REPO) +
+                                " (ALU opcodes x 32 lanes from the ncu SASS mix; 64 lanes/clk/SM measured)")
+        except Exception:
+            continue
+    return None
+
+
 class ClockSampler:
     """Samples SM clocks and throttle reasons with NVML while the timed region runs."""
 
@@ -429,7 +445,21 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
                 "kernel_ms": round(kernel_ms, 5),
                 "kernel_ms_min": round(min(per), 5)}
     if prof.get("alu"):
-        roofline["alu"] = prof["alu"]
+        roofline["alu"] = dict(prof["alu"])
+    alu = read_alu_floor(cfg.name)
+    if alu:
+        # the binding roofline for every config (ALU floor > HBM floor): ALU-pipe lane-ops per
+        # pixel are a property of the kernel and the scene (counted from the ncu SASS mix of
+        # the committed capture), the time is this run's per-launch kernel time
+        ops = alu["alu_lane_ops_per_px"] * batch_px
+        peak_alu = 64 * 148 * 1.965e9
+        roofline.setdefault("alu", {}).update({
+            "lane_ops_per_px": round(alu["alu_lane_ops_per_px"], 2),
+            "achieved_Tops": round(ops / (kernel_ms * 1e-3) / 1e12, 3),
+            "peak_Tops": round(peak_alu / 1e12, 3),
+            "frac": round(ops / (kernel_ms * 1e-3) / peak_alu, 4),
+            "floor_us": round(ops / peak_alu * 1e6, 2),
+            "source": alu["source"]})
 
     # e2e through the C-ABI host entry: pinned host in/out, H2D + filter + D2H each step
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(steps, 20 if batch_bytes > (256 << 20) else 50))
