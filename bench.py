@@ -445,7 +445,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
                 "kernel_ms": round(kernel_ms, 5),
                 "kernel_ms_min": round(min(per), 5)}
     if prof.get("alu"):
-        roofline["alu"] = dict(prof["alu"])
+        roofline["alu"] = {k: v for k, v in prof["alu"].items() if v is not None}
     alu = read_alu_floor(cfg.name)
     if alu:
         # the binding roofline for every config (ALU floor > HBM floor): ALU-pipe lane-ops per

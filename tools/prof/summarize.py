@@ -105,7 +105,6 @@ def main():
             "algorithmic_bytes_per_launch": alg,
             "traffic_over_algorithmic": (dram / alg) if dram == dram else None,
             "alu": {"bound": "alu", "pipe_utilisation_pct": alu_pct,
-                    "alu_warp_inst_per_px": (alu_inst / px) if alu_inst == alu_inst else None,
                     "thread_inst_per_px": inst * 32 / px,
                     "peak_lanes_per_clk_per_sm": PEAK_ALU_LANES_PER_CLK_SM,
                     "source": f"ncu --set full, profiles/ncu_{tag}_{cfg}.txt"},
