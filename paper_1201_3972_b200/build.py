@@ -22,9 +22,9 @@ CUDA_HEADERS = ["fnr_common.cuh", "fnr_generic.cuh", "fnr_fast.cuh", "fnr_tile.c
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-fvisibility=hidden",
+    "-Xcompiler", "-fPIC,-fvisibility=hidden,-fopenmp",
     "-Xptxas", "-v",
-    "-shared", "-cudart", "static",
+    "-shared", "-cudart", "static", "-lgomp",
 ]
 
 

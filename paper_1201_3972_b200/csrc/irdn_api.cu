@@ -204,9 +204,56 @@ struct DeviceWorkspace {
   unsigned long long* counts = nullptr;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_done;  // grow-only pools (created once, reused per call)
+  // pageable host buffers: pinned staging slots (in / out), CPU copies run in parallel
+  // (OpenMP) while the DMA engines move the neighbouring chunks
+  void* stage_in = nullptr;
+  void* stage_out = nullptr;
+  size_t stage_cap = 0;  // bytes per direction (kStageSlots slots)
+  cudaEvent_t ev_out[4] = {nullptr, nullptr, nullptr, nullptr};
   bool ready = false;
 };
+constexpr int kStageSlots = 3;
 static DeviceWorkspace g_ws[64];
+
+static int ensure_staging(DeviceWorkspace& ws, size_t slot_bytes) {
+  const size_t need = slot_bytes * kStageSlots;
+  if (ws.stage_cap < need) {
+    if (ws.stage_in) IRDN_CUDA(cudaFreeHost(ws.stage_in));
+    if (ws.stage_out) IRDN_CUDA(cudaFreeHost(ws.stage_out));
+    ws.stage_in = ws.stage_out = nullptr;
+    ws.stage_cap = 0;
+    IRDN_CUDA(cudaHostAlloc(&ws.stage_in, need, cudaHostAllocDefault));
+    IRDN_CUDA(cudaHostAlloc(&ws.stage_out, need, cudaHostAllocDefault));
+    ws.stage_cap = need;
+  }
+  for (int i = 0; i < kStageSlots; ++i)
+    if (!ws.ev_out[i]) IRDN_CUDA(cudaEventCreateWithFlags(&ws.ev_out[i], cudaEventDisableTiming));
+  return IRDN_OK;
+}
+
+// memcpy split over the OpenMP team (host DRAM bandwidth, not one core, bounds it)
+static void par_copy(void* dst, const void* src, size_t n) {
+  constexpr size_t kPart = 256 << 10;
+  const long long parts = (long long)((n + kPart - 1) / kPart);
+  if (parts <= 1) {
+    memcpy(dst, src, n);
+    return;
+  }
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < parts; ++i) {
+    const size_t off = (size_t)i * kPart;
+    memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, std::min(kPart, n - off));
+  }
+}
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
 
 static int ensure_workspace(DeviceWorkspace& ws, size_t bytes) {
   if (!ws.ready) {
@@ -292,16 +339,62 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   std::vector<cudaEvent_t>& ev_done = ws.ev_done;
 
   const bool row_mode = batch == 1 && chunks.size() > 1;
+  auto chunk_off = [&](const Chunk& c) { return c.f0 * frame + c.y0 * width; };
+  auto chunk_cnt = [&](const Chunk& c) { return row_mode ? (c.y1 - c.y0) * width : c.nf * frame; };
+  // Pageable caller buffers: DMA from / to pinned staging slots; the CPU copies chunk
+  // i into a slot (parallel memcpy) while the copy engines move chunks i-1 and i-2.
+  const bool staged_in = !is_pinned(h_in), staged_out = !is_pinned(h_out);
+  const bool staged = staged_in || staged_out;
+  int64_t max_cnt = 0;
+  for (const Chunk& c : chunks) max_cnt = std::max(max_cnt, chunk_cnt(c));
+  const size_t slot_bytes = ((size_t)max_cnt * sizeof(T) + 255) & ~(size_t)255;
+  if (staged && (rc = ensure_staging(ws, slot_bytes))) return rc;
+  auto stage_in = [&](size_t i) { return reinterpret_cast<T*>(static_cast<char*>(ws.stage_in) + (i % kStageSlots) * slot_bytes); };
+  auto stage_out = [&](size_t i) { return reinterpret_cast<T*>(static_cast<char*>(ws.stage_out) + (i % kStageSlots) * slot_bytes); };
+  auto drain_out = [&](size_t i) -> int {  // chunk i's D2H into its slot -> caller's buffer
+    IRDN_CUDA(cudaEventSynchronize(ws.ev_out[i % kStageSlots]));
+    par_copy(h_out + chunk_off(chunks[i]), stage_out(i), (size_t)chunk_cnt(chunks[i]) * sizeof(T));
+    return IRDN_OK;
+  };
   // H2D: each chunk's own rows (row mode: strips, in order).
-  for (size_t i = 0; i < chunks.size(); ++i) {
-    const Chunk& c = chunks[i];
-    const int64_t off = c.f0 * frame + c.y0 * width;
-    const int64_t cnt = row_mode ? (c.y1 - c.y0) * width : c.nf * frame;
-    IRDN_CUDA(cudaMemcpyAsync(d_in + off, h_in + off, cnt * sizeof(T), cudaMemcpyHostToDevice, ws.s_h2d));
-    IRDN_CUDA(cudaEventRecord(ev_in[i], ws.s_h2d));
+  if (!staged_in) {
+    for (size_t i = 0; i < chunks.size(); ++i) {
+      const int64_t off = chunk_off(chunks[i]), cnt = chunk_cnt(chunks[i]);
+      IRDN_CUDA(cudaMemcpyAsync(d_in + off, h_in + off, cnt * sizeof(T), cudaMemcpyHostToDevice, ws.s_h2d));
+      IRDN_CUDA(cudaEventRecord(ev_in[i], ws.s_h2d));
+    }
   }
+  size_t drained = 0, issued = 0;
+  // staged H2D of chunks [issued, upto]: slot j % kStageSlots was last used by chunk
+  // j - kStageSlots, whose H2D must be done before the slot is refilled and whose output
+  // must be copied out before the D2H reuses the slot (its D2H is already enqueued: a
+  // row strip looks ahead at most one strip, kStageSlots >= 3)
+  auto issue_h2d = [&](size_t upto) -> int {
+    for (; issued <= upto && issued < chunks.size(); ++issued) {
+      const size_t j = issued;
+      if (j >= (size_t)kStageSlots) {
+        IRDN_CUDA(cudaEventSynchronize(ev_in[j - kStageSlots]));
+        if (staged_out && drained <= j - kStageSlots) {
+          int e = drain_out(j - kStageSlots);
+          if (e) return e;
+          drained = j - kStageSlots + 1;
+        }
+      }
+      const int64_t off = chunk_off(chunks[j]), cnt = chunk_cnt(chunks[j]);
+      par_copy(stage_in(j), h_in + off, (size_t)cnt * sizeof(T));
+      IRDN_CUDA(cudaMemcpyAsync(d_in + off, stage_in(j), cnt * sizeof(T), cudaMemcpyHostToDevice, ws.s_h2d));
+      IRDN_CUDA(cudaEventRecord(ev_in[j], ws.s_h2d));
+    }
+    return IRDN_OK;
+  };
   for (size_t i = 0; i < chunks.size(); ++i) {
     const Chunk& c = chunks[i];
+    if (staged_in) {
+      size_t need = i;
+      if (row_mode)
+        while (need + 1 < chunks.size() && chunks[need].y1 < std::min<int64_t>(height, c.y1 + r)) ++need;
+      if ((rc = issue_h2d(need))) return rc;
+    }
     if (row_mode) {
       // A strip needs the input rows up to y1 + r, i.e. possibly the next chunk's copy.
       size_t last = i;
@@ -321,10 +414,18 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
     }
     IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
     IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
-    const int64_t off = c.f0 * frame + c.y0 * width;
-    const int64_t cnt = row_mode ? (c.y1 - c.y0) * width : c.nf * frame;
-    IRDN_CUDA(cudaMemcpyAsync(h_out + off, d_out + off, cnt * sizeof(T), cudaMemcpyDeviceToHost, ws.s_d2h));
+    const int64_t off = chunk_off(c), cnt = chunk_cnt(c);
+    if (staged_out && !staged_in && i >= (size_t)kStageSlots && drained <= i - kStageSlots) {
+      if ((rc = drain_out(i - kStageSlots))) return rc;  // the slot's previous chunk
+      drained = i - kStageSlots + 1;
+    }
+    IRDN_CUDA(cudaMemcpyAsync(staged_out ? stage_out(i) : h_out + off, d_out + off, cnt * sizeof(T),
+                              cudaMemcpyDeviceToHost, ws.s_d2h));
+    if (staged_out) IRDN_CUDA(cudaEventRecord(ws.ev_out[i % kStageSlots], ws.s_d2h));
   }
+  if (staged_out)
+    for (size_t i = drained; i < chunks.size(); ++i)
+      if ((rc = drain_out(i))) return rc;
   unsigned long long counts[2] = {0, 0};
   IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[chunks.size() - 1], 0));
   IRDN_CUDA(cudaMemcpyAsync(counts, ws.counts, sizeof(counts), cudaMemcpyDeviceToHost, ws.s_d2h));

@@ -337,3 +337,33 @@ def test_cta_tile_kernel_family_matches_oracle(cuda_ok, tmp_path):
     env = dict(os.environ, IRDN_KERNEL="tile")
     out = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=600)
     assert out.returncode == 0 and "tile ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("in_pinned,out_pinned", [(False, False), (True, False), (False, True), (True, True)])
+def test_host_entry_pinned_and_pageable_buffers(cuda_ok, in_pinned, out_pinned):
+    """irdn_run_filter_*: pinned caller buffers are DMA'd directly, pageable ones go through
+    the pinned staging slots (parallel CPU copies) — every combination, batch chunking and
+    single-frame row strips, gives the device-path result."""
+    import torch
+
+    lib = _native.load_lib()
+
+    def buf(a, pinned):
+        if not pinned:
+            return np.ascontiguousarray(a), None
+        t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+        v = t.numpy().view(a.dtype).reshape(a.shape)
+        v[...] = a
+        return v, t
+
+    cases = [(generate(CONFIGS["c2"].with_shape(height=256, width=320), nframes=40), 5),  # 6.5 MB chunks
+             (generate(CONFIGS["c4"].with_shape(height=3072, width=3072), nframes=1)[0], 11)]  # 18 MB: strips
+    for img, k in cases:
+        want, wst = _oracle(img, k, "fnr", 1)
+        src, keep_in = buf(img, in_pinned)
+        out, keep_out = buf(np.zeros_like(img), out_pinned)
+        st = _native.IrdnStats()
+        b, h, w = (1,) + img.shape if img.ndim == 2 else img.shape
+        _native.check(lib.irdn_run_filter_u16(src.ctypes.data, out.ctypes.data, b, h, w, k, 0, 1, 0, ctypes.byref(st)))
+        assert np.array_equal(out, want), (img.shape, in_pinned, out_pinned)
+        assert counters(st) == wst
