@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <omp.h>
 #include <string>
 #include <vector>
 
@@ -239,7 +240,13 @@ static void par_copy(void* dst, const void* src, size_t n) {
     memcpy(dst, src, n);
     return;
   }
-#pragma omp parallel for schedule(static)
+  // a few threads saturate host DRAM for a copy; more only oversubscribe the host when
+  // one process per GPU runs (8 ranks on one node)
+  static const int nt = [] {
+    const char* e = getenv("IRDN_COPY_THREADS");
+    return std::max(1, e ? atoi(e) : std::min(8, omp_get_max_threads()));
+  }();
+#pragma omp parallel for schedule(static) num_threads(nt)
   for (long long i = 0; i < parts; ++i) {
     const size_t off = (size_t)i * kPart;
     memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, std::min(kPart, n - off));
