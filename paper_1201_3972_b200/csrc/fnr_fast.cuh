@@ -198,6 +198,7 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
       cudaGetLastError();
       n = 1;
     }
+    if (getenv("IRDN_WARP_CTAS")) n = std::min(n, atoi(getenv("IRDN_WARP_CTAS")));  // experiments
     blocks_per_sm = n;
   }
   int dev = 0, sms = 148;
