@@ -367,3 +367,31 @@ def test_host_entry_pinned_and_pageable_buffers(cuda_ok, in_pinned, out_pinned):
         _native.check(lib.irdn_run_filter_u16(src.ctypes.data, out.ctypes.data, b, h, w, k, 0, 1, 0, ctypes.byref(st)))
         assert np.array_equal(out, want), (img.shape, in_pinned, out_pinned)
         assert counters(st) == wst
+
+
+def test_randomized_shapes_windows_methods(cuda_ok):
+    """Seeded fuzz: random batch / shape / window / dtype / method / passes / value
+    distribution (incl. low-entropy images with many ties), GPU vs oracle, bit-exact pixels
+    and counters. Shapes straddle the tile sizes (64x32 warp tiles, 128-wide 3x3 tiles,
+    16-byte alignment of rows) so partial tiles, generic fallbacks and edge fix-ups all run."""
+    rng = np.random.default_rng(20261020)
+    for case in range(60):
+        dtype = np.uint8 if rng.random() < 0.5 else np.uint16
+        k = int(rng.choice([3, 5, 7, 9, 11, 13]))
+        b = int(rng.integers(1, 4))
+        h = int(rng.integers(1, 150))
+        w = int(rng.choice([int(rng.integers(1, 40)), int(rng.integers(40, 300)), 64, 128, 256]))
+        hi = int(rng.choice([2, 4, 256, 65536 if dtype == np.uint16 else 256]))
+        img = rng.integers(0, hi, size=(b, h, w)).astype(dtype)
+        if rng.random() < 0.3:  # smooth field + impulses
+            yy, xx = np.mgrid[0:h, 0:w]
+            base = (yy * 3 + xx * 2) % (250 if dtype == np.uint8 else 16000)
+            img = np.broadcast_to(base, (b, h, w)).astype(dtype).copy()
+            m = rng.random(img.shape) < 0.3
+            img[m] = rng.integers(0, 256 if dtype == np.uint8 else 65536, int(m.sum())).astype(dtype)
+        method = "mf" if rng.random() < 0.25 else "fnr"
+        passes = int(rng.choice([1, 1, 2, 3]))
+        want, wst = _oracle(img, k, method, passes)
+        got, gst = gpu_filter(img, k, method, passes)
+        assert np.array_equal(got, want), (case, dtype, k, img.shape, method, passes)
+        assert gst == wst, (case, gst, wst)
