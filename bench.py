@@ -430,8 +430,12 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
             launch(i)
             evs[i][1].record(stream)
     torch.cuda.synchronize(dev)
-    per = [a.elapsed_time(b) / passes for a, b in evs]  # per filter launch
-    kernel_ms = statistics.mean(per)
+    per = [a.elapsed_time(b) / passes for a, b in evs]  # per filter launch, isolated by events
+    # the dominant kernel's average launch duration over the timed region: the region
+    # holds exactly steps x passes filter launches back to back (programmatic dependent
+    # launch overlaps each launch's ramp with the previous one's tail); the isolated
+    # per-launch figure (events around every launch defeat that overlap) is kept beside it
+    kernel_ms = elapsed_ms / (steps * passes)
 
     peak, peak_src = read_peaks()
     alg_bytes = batch_px * 2 * bpp
@@ -443,7 +447,9 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "bytes_per_pixel": 2 * bpp, "pixels_per_launch": batch_px,
                 "kernel_ms": round(kernel_ms, 5),
-                "kernel_ms_min": round(min(per), 5)}
+                "kernel_ms_source": "CUDA events over the timed region / filter launches in it",
+                "kernel_ms_isolated": round(statistics.mean(per), 5),
+                "kernel_ms_isolated_min": round(min(per), 5)}
     if prof.get("alu"):
         roofline["alu"] = {k: v for k, v in prof["alu"].items() if v is not None}
     alu = read_alu_floor(cfg.name)
