@@ -150,12 +150,12 @@ __device__ __forceinline__ void store_pair_g(T* dst, uint32_t v, bool ok0, bool 
 }
 
 template <int NV>
-__device__ __forceinline__ uint32_t median_dispatch(uint32_t (&v)[NV]) {
-  if constexpr (NV == 9) return median_net_9(v);
-  else if constexpr (NV == 25) return median_net_25(v);
-  else if constexpr (NV == 49) return median_net_49(v);
-  else if constexpr (NV == 81) return median_net_81(v);
-  else return median_net_121(v);
+__device__ __forceinline__ uint32_t median_dispatch(uint32_t (&v)[NV], uint32_t m1) {
+  if constexpr (NV == 9) return median_net_9(v, m1);
+  else if constexpr (NV == 25) return median_net_25(v, m1);
+  else if constexpr (NV == 49) return median_net_49(v, m1);
+  else if constexpr (NV == 81) return median_net_81(v, m1);
+  else return median_net_121(v, m1);
 }
 
 // Min / max of N packed words with 3-input VIMNMX3 (N odd: (N-1)/2 instructions).
@@ -232,7 +232,7 @@ __device__ __forceinline__ void fix_edges(T* s_in, int gx_lo, int gy_lo, int wid
 // medians overwrite the copied centres at out_tile. Returns this lane's replacements.
 template <typename T, int K>
 __device__ __forceinline__ uint32_t median_queue(const T* s_in, const uint16_t* q, int n, T* out_tile,
-                                                 int64_t pitch, int lane, bool fnr) {
+                                                 int64_t pitch, int lane, bool fnr, uint32_t m1) {
   using G = Geo<T, K>;
   constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
   uint32_t replaced = 0;
@@ -252,11 +252,11 @@ __device__ __forceinline__ uint32_t median_queue(const T* s_in, const uint16_t* 
 #pragma unroll
       for (int dx = 0; dx < K; ++dx)
         v[dy * K + dx] = (uint32_t)a[dy * BOXW + dx] | ((uint32_t)bb[dy * BOXW + dx] << 16);
-    const uint32_t med = skip_net ? (v[0] ^ v[K * K - 1] ^ v[K * K / 2]) : median_dispatch<K * K>(v);
-    const uint32_t m0 = med & 0xFFFFu, m1 = med >> 16;
-    out_tile[y0 * pitch + x0] = (T)m0;
-    if (two) out_tile[y1 * pitch + x1] = (T)m1;
-    if (fnr) replaced += (m0 != (uint32_t)a[r * BOXW + r]) + (two && m1 != (uint32_t)bb[r * BOXW + r]);
+    const uint32_t med = skip_net ? (v[0] ^ v[K * K - 1] ^ v[K * K / 2]) : median_dispatch<K * K>(v, m1);
+    const uint32_t med0 = med & 0xFFFFu, med1 = med >> 16;
+    out_tile[y0 * pitch + x0] = (T)med0;
+    if (two) out_tile[y1 * pitch + x1] = (T)med1;
+    if (fnr) replaced += (med0 != (uint32_t)a[r * BOXW + r]) + (two && med1 != (uint32_t)bb[r * BOXW + r]);
   }
   return replaced;
 }
@@ -446,7 +446,8 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
         }
       }
       __syncwarp();  // queue visible; centre stores ordered before the median stores
-      if (p.debug != 1) replaced += median_queue<T, K>(s_in, s_q, p.debug == 2 ? -n : n, out_tile, p.out_pitch, lane, true);
+      if (p.debug != 1) replaced += median_queue<T, K>(s_in, s_q, p.debug == 2 ? -n : n, out_tile, p.out_pitch, lane, true,
+                                                          0u - p.one);
       __syncwarp();
     } else {
       // MF: every valid pixel of the strip through the same queue
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(THREADS) fnr_tile_kernel(const __grid_constant
         s_q[j] = (uint16_t)(((band0 + y) << 8) | ((warp & 1) * 64 + x));
       }
       __syncwarp();
-      median_queue<T, K>(s_in, s_q, n, out_tile, p.out_pitch, lane, false);
+      median_queue<T, K>(s_in, s_q, n, out_tile, p.out_pitch, lane, false, 0u - p.one);
       __syncwarp();
     }
     // all warps are done with this stage: refill it with the next tile

@@ -173,7 +173,7 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
 // Median of queued pixels (entries y << 8 | x in warp-tile coords), two per lane.
 template <typename T, int K>
 __device__ __forceinline__ uint32_t medians(const T* s_in, const uint16_t* q, int n, T* out_tile, int64_t pitch,
-                                            int lane, bool fnr) {
+                                            int lane, bool fnr, uint32_t m1) {
   using G = Geo<T, K>;
   constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
   uint32_t replaced = 0;
@@ -199,11 +199,11 @@ __device__ __forceinline__ uint32_t medians(const T* s_in, const uint16_t* q, in
 #pragma unroll
       for (int dx = 0; dx < K; ++dx)
         v[dy * K + dx] = (uint32_t)a[dy * BOXW + dx] | ((uint32_t)bb[dy * BOXW + dx] << 16);
-    const uint32_t med = tile::median_dispatch<K * K>(v);
-    const uint32_t m0 = med & 0xFFFFu, m1 = med >> 16;
-    out_tile[y0 * pitch + x0] = (T)m0;
-    if (two) out_tile[y1 * pitch + x1] = (T)m1;
-    if (fnr) replaced += (m0 != (uint32_t)a[r * BOXW + r]) + (two && m1 != (uint32_t)bb[r * BOXW + r]);
+    const uint32_t med = tile::median_dispatch<K * K>(v, m1);
+    const uint32_t med0 = med & 0xFFFFu, med1 = med >> 16;
+    out_tile[y0 * pitch + x0] = (T)med0;
+    if (two) out_tile[y1 * pitch + x1] = (T)med1;
+    if (fnr) replaced += (med0 != (uint32_t)a[r * BOXW + r]) + (two && med1 != (uint32_t)bb[r * BOXW + r]);
   }
   return replaced;
 }
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
           }
         }
         __syncwarp();  // queue visible; centre stores ordered before the median stores
-        replaced += medians<T, K>(s_in, s_q, min(QCAP, n - q0), out_tile, p.out_pitch, lane, true);
+        replaced += medians<T, K>(s_in, s_q, min(QCAP, n - q0), out_tile, p.out_pitch, lane, true, 0u - p.one);
         __syncwarp();  // queue reads done before the next round overwrites it
       }
     } else {
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
           s_q[j] = (uint16_t)((y << 8) | x);
         }
         __syncwarp();
-        medians<T, K>(s_in, s_q, min(QCAP, n - q0), out_tile, p.out_pitch, lane, false);
+        medians<T, K>(s_in, s_q, min(QCAP, n - q0), out_tile, p.out_pitch, lane, false, 0u - p.one);
         __syncwarp();
       }
     }

@@ -49,6 +49,9 @@ __global__ void alu_kernel(uint32_t* out, uint32_t seed) {
       if (OP == 15) { uint32_t t; if (i & 1) asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(v[i]), "r"(c), "r"(v[(i + 1) % CHAINS])); else asm volatile("{.reg .b32 q; min.u16x2 q, %1, %2; min.u16x2 %0, q, %3;}" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS]), "r"(b)); v[i] = t; }  // VIMNMX3 + IMAD
       if (OP == 16) { uint32_t t; asm volatile("add.u32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); asm volatile("add.u32 %0, %0, %1;" : "+r"(t) : "r"(b)); v[i] = t; }  // IADD3
       if (OP == 7) { uint32_t t; asm volatile("min.u32 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // IMNMX.U32
+      if (OP == 17) { uint32_t t; if (i & 1) asm volatile("{.reg .b32 q; add.u32 q, %1, %2; sub.u32 %0, q, %3;}" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS]), "r"(b)); else asm volatile("min.u16x2 %0, %1, %2;" : "=r"(t) : "r"(v[i]), "r"(v[(i + 1) % CHAINS])); v[i] = t; }  // VIMNMX + IADD3 a+b-c
+      if (OP == 18) { const uint32_t a = v[i], bb = v[(i + 1) % CHAINS]; uint32_t lo, hi; asm volatile("min.u16x2 %0, %1, %2;" : "=r"(lo) : "r"(a), "r"(bb)); asm volatile("{.reg .b32 q; add.u32 q, %1, %2; sub.u32 %0, q, %3;}" : "=r"(hi) : "r"(a), "r"(bb), "r"(lo)); v[i] = lo; v[(i + 1) % CHAINS] = hi; }  // cx as min + (a+b-min)
+      if (OP == 19) { const uint32_t a = v[i], bb = v[(i + 1) % CHAINS]; uint32_t lo, hi; asm volatile("min.u16x2 %0, %1, %2;" : "=r"(lo) : "r"(a), "r"(bb)); asm volatile("max.u16x2 %0, %1, %2;" : "=r"(hi) : "r"(a), "r"(bb)); v[i] = lo; v[(i + 1) % CHAINS] = hi; }  // cx as min + max
     }
   }
   uint32_t acc = 0;
@@ -109,6 +112,9 @@ int main() {
   run_alu<14>("imad_hi_plus_lop3", 2);
   run_alu<15>("mixed_vimnmx3_imad", 1);
   run_alu<16>("iadd3_3input", 1);
+  run_alu<17>("mixed_vimnmx_iadd3_sub", 1);
+  run_alu<18>("cx_min_plus_addsub", 2);
+  run_alu<19>("cx_min_max", 2);
 
   // HBM copy: 2 GiB in + 2 GiB out
   size_t bytes = (size_t)2 << 30;

@@ -17,7 +17,13 @@ sm_100a), so one network evaluation selects the medians of two windows.
 Checks: 0-1 principle exhaustively for n <= 25 (bit-parallel), random
 multisets for larger n.
 
-    python tools/netgen/netgen.py > paper_1201_3972_b200/csrc/select_nets.cuh
+    python tools/netgen/netgen.py --addsub=49:120 > paper_1201_3972_b200/csrc/select_nets.cuh
+
+`--addsub=n:count` forms `count` of the n-input network's compare-exchange maxima as
+a + b - min (IADD + IMAD on the FMA pipe) instead of a second VIMNMX: it trades ALU-pipe
+ops for issue slots, which pays only where the median network is ALU-bound — measured
+for 7x7 (c3: 714 -> 690 us at 120 of 232 candidates; all 232 -> 751 us, issue-bound),
+not for 5x5 (c2) or 11x11 (c4), which stay plain.
 """
 
 from __future__ import annotations
@@ -240,7 +246,7 @@ def check(n, ops, out_slot):
         assert evaluate(ops, out_slot, vals) == sorted(vals)[rank], f"random check failed n={n}"
 
 
-def to_ssa(n, ops, out_slot):
+def to_ssa(n, ops, out_slot, addsub: int = 0):
     """Lower a slot network to SSA instructions and fuse single-use min->min / max->max
     chains into 3-input min/max (VIMNMX3.U16x2 on sm_100a).
 
@@ -303,30 +309,59 @@ def to_ssa(n, ops, out_slot):
                         break
             if changed:
                 break
-    return [(o, instrs[o][0], instrs[o][1]) for o in order], result
+    out = [(o, instrs[o][0], instrs[o][1]) for o in order]
+    if addsub:
+        # compare-exchange whose min and max both survive as 2-input ops: keep the min on
+        # the ALU pipe and form the max as a + b - min (exact on packed u16x2 words: each
+        # lane of a + b - min is that lane's max, so no borrow crosses lanes) with one IADD
+        # and one IMAD, which issue on the FMA pipe; `addsub` of them are converted
+        mins = {}
+        for name, kind, srcs in out:
+            if kind == "min" and len(srcs) == 2:
+                mins.setdefault(frozenset(srcs), name)
+        conv = 0
+        for i, (name, kind, srcs) in enumerate(out):
+            if conv >= addsub:
+                break
+            if kind == "max" and len(srcs) == 2 and frozenset(srcs) in mins:
+                lo = mins[frozenset(srcs)]
+                if order.index(lo) < order.index(name):
+                    out[i] = (name, "addsub", [srcs[0], srcs[1], lo])
+                    conv += 1
+    return out, result
 
 
 def eval_ssa(instrs, result, values):
     env = {f"x{i}": v for i, v in enumerate(values)}
     for name, kind, srcs in instrs:
         vals = [env[s] for s in srcs]
-        env[name] = min(vals) if kind == "min" else max(vals)
+        if kind == "addsub":
+            env[name] = vals[0] + vals[1] - vals[2]
+        else:
+            env[name] = min(vals) if kind == "min" else max(vals)
     return env[result]
 
 
-def emit(n, ops, out_slot) -> str:
-    instrs, result = to_ssa(n, ops, out_slot)
+def emit(n, ops, out_slot, addsub: int = 0) -> str:
+    instrs, result = to_ssa(n, ops, out_slot, addsub)
     rng = random.Random(7)
     for _ in range(3000):
         vals = [rng.randrange(0, rng.choice([2, 3, 16, 65536])) for _ in range(n)]
         assert eval_ssa(instrs, result, vals) == sorted(vals)[(n - 1) // 2]
-    n3 = sum(1 for _, _, s in instrs if len(s) == 3)
-    lines = [f"// median of {n} values: {len(ops)} comparators -> {len(instrs)} packed u16x2 "
-             f"min/max instructions ({n3} of them 3-input)",
-             f"__device__ __forceinline__ uint32_t median_net_{n}(const uint32_t (&x)[{n}]) {{"]
+    n3 = sum(1 for _, k, s in instrs if len(s) == 3 and k != "addsub")
+    nas = sum(1 for _, k, _ in instrs if k == "addsub")
+    lines = [f"// median of {n} values: {len(ops)} comparators -> {len(instrs) - nas} packed u16x2 "
+             f"min/max instructions ({n3} of them 3-input)"
+             + (f" + {nas} maxima as a + b - min (IADD + IMAD)" if nas else ""),
+             f"__device__ __forceinline__ uint32_t median_net_{n}(const uint32_t (&x)[{n}], uint32_t m1) {{"]
+    if not nas:
+        lines.append("  (void)m1;")
     for i in range(n):
         lines.append(f"  const uint32_t x{i} = x[{i}];")
     for name, kind, srcs in instrs:
+        if kind == "addsub":
+            lines.append(f"  const uint32_t {name} = addsub({srcs[0]}, {srcs[1]}, {srcs[2]}, m1);")
+            continue
         fn = ("vmin" if kind == "min" else "vmax") + str(len(srcs))
         lines.append(f"  const uint32_t {name} = {fn}({', '.join(srcs)});")
     lines.append(f"  return {result};")
@@ -335,7 +370,14 @@ def emit(n, ops, out_slot) -> str:
 
 
 def main():
-    sizes = [int(a) for a in sys.argv[1:]] or [9, 25, 49, 81, 121]
+    args = [a for a in sys.argv[1:] if not a.startswith("--addsub=")]
+    addsub = {}
+    for a in sys.argv[1:]:
+        if a.startswith("--addsub="):  # --addsub=49:160,121:0  (maxima per network as a + b - min)
+            for kv in a.split("=", 1)[1].split(","):
+                k, v = kv.split(":")
+                addsub[int(k)] = int(v)
+    sizes = [int(a) for a in args] or [9, 25, 49, 81, 121]
     out = ["// GENERATED by tools/netgen/netgen.py — do not edit.",
            "// Exact median-selection networks (pruned Batcher odd-even merge sort) on packed",
            "// u16x2 words: each op is one VIMNMX.U16x2, so one call yields two medians.",
@@ -352,13 +394,19 @@ def main():
            "}",
            "__device__ __forceinline__ uint32_t vmax3(uint32_t a, uint32_t b, uint32_t c) {",
            "  uint32_t r; asm(\"{.reg .b32 t; max.u16x2 t, %1, %2; max.u16x2 %0, t, %3;}\" : \"=r\"(r) : \"r\"(a), \"r\"(b), \"r\"(c)); return r;",
+           "}",
+           "// max(a, b) given lo = min(a, b): a + b - lo, lane-exact on packed words; the add is a",
+           "// 2-input IADD (either pipe) and the subtract an IMAD with the opaque m1 = -1 (FMA pipe)",
+           "__device__ __forceinline__ uint32_t addsub(uint32_t a, uint32_t b, uint32_t lo, uint32_t m1) {",
+           "  uint32_t s, r; asm(\"add.u32 %0, %1, %2;\" : \"=r\"(s) : \"r\"(a), \"r\"(b));",
+           "  asm(\"mad.lo.u32 %0, %1, %2, %3;\" : \"=r\"(r) : \"r\"(lo), \"r\"(m1), \"r\"(s)); return r;",
            "}", ""]
     iters = {9: 400, 25: 1500, 49: 800, 81: 200, 121: 150}
     for n in sizes:
         _, ops, slot, base_name = search(n, (n - 1) // 2, iters.get(n, 100))
         check(n, ops, slot)
         sys.stderr.write(f"n={n}: base {base_name}\n")
-        text = emit(n, ops, slot)
+        text = emit(n, ops, slot, addsub.get(n, 0))
         sys.stderr.write(f"n={n}: {len(ops)} comparators -> {text.splitlines()[0]}\n")
         out.append(text)
         out.append("")
