@@ -395,3 +395,19 @@ def test_randomized_shapes_windows_methods(cuda_ok):
         got, gst = gpu_filter(img, k, method, passes)
         assert np.array_equal(got, want), (case, dtype, k, img.shape, method, passes)
         assert gst == wst, (case, gst, wst)
+
+
+def test_fnr_pass_mf_pass_accumulate_like_the_reference(cuda_ok):
+    """fnr_pass / mf_pass (filters.py:69-76): one pass each, counters (passes included)
+    added to the caller's FilterStats, elapsed_ms untouched; two chained fnr_pass calls
+    equal run_filter(passes=2) pixel for pixel and counter for counter."""
+    for meta, inp, out in load_golden("ref_fixtures.npz")[:6]:
+        h, w = inp.shape
+        img = P.GrayImage(w, h, inp.tobytes())
+        st = P.FilterStats(elapsed_ms=12.5)
+        step = P.fnr_pass if meta["method"] == "fnr" else P.mf_pass
+        cur = img
+        for _ in range(meta["passes"]):
+            cur = step(cur, P.WindowSpec(meta["k"]), st)
+        assert bytes(cur.pixels) == out.tobytes(), meta
+        assert counters(st) == meta["stats"] and st.elapsed_ms == 12.5, (meta, st)
