@@ -466,6 +466,14 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
             "frac": round(ops / (kernel_ms * 1e-3) / peak_alu, 4),
             "floor_us": round(ops / peak_alu * 1e6, 2),
             "source": alu["source"]})
+        if "instr_per_px" in alu:
+            # issue roofline: every instruction needs an issue slot (4 per clk per SM)
+            instr = alu["instr_per_px"] * batch_px
+            peak_issue = 128 * 148 * 1.965e9
+            roofline["issue"] = {"instr_per_px": round(alu["instr_per_px"], 2),
+                                 "floor_us": round(instr / peak_issue * 1e6, 2),
+                                 "frac": round(instr / (kernel_ms * 1e-3) / peak_issue, 4),
+                                 "peak_Tinstr": round(peak_issue / 1e12, 3)}
 
     # e2e through the C-ABI host entry: pinned host in/out, H2D + filter + D2H each step
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(steps, 20 if batch_bytes > (256 << 20) else 50))

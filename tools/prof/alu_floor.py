@@ -16,6 +16,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 ALU_OPS = ("VIMNMX", "VIMNMX3", "IMNMX", "FMNMX", "HMNMX2", "LOP3", "LOP", "PRMT", "ISETP", "SEL", "SHF", "FLO",
            "POPC", "BREV", "PLOP3", "FSEL", "SGXT", "BMSK", "VABSDIFF", "VABSDIFF4", "ISCADD")
 PEAK = 64 * 148 * 1.965e9  # ALU lane-ops / s
+ISSUE = 128 * 148 * 1.965e9  # thread-instructions / s (4 schedulers x 1 warp-instr / clk / SM)
 HBM = 6555.5e9
 
 
@@ -53,15 +54,19 @@ def main():
         t_alu = alu * 32 / PEAK * 1e6
         t_hbm = b["roofline"]["algorithmic_bytes_per_launch"] / HBM * 1e6
         k = b["roofline"]["kernel_ms"] * 1e3
+        t_issue = tot * 32 / ISSUE * 1e6
         rows.append(dict(config=c, alu_lane_ops_per_px=alu * 32 / px, instr_per_px=tot * 32 / px,
-                         alu_floor_us=t_alu, hbm_floor_us=t_hbm, kernel_us=k, alu_frac=t_alu / k, hbm_frac=t_hbm / k))
+                         alu_floor_us=t_alu, issue_floor_us=t_issue, hbm_floor_us=t_hbm, kernel_us=k,
+                         alu_frac=t_alu / k, issue_frac=t_issue / k, hbm_frac=t_hbm / k))
     path = os.path.join(REPO, "profiles", f"alu_floor_{tag}.json")
     json.dump(rows, open(path, "w"), indent=1)
-    print("| config | ALU ops/px | instr/px | ALU floor us | HBM floor us | kernel us | ALU frac | HBM frac |")
-    print("|---|---|---|---|---|---|---|---|")
+    print("| config | ALU ops/px | instr/px | ALU floor us | issue floor us | HBM floor us | kernel us | "
+          "ALU frac | issue frac | HBM frac |")
+    print("|---|---|---|---|---|---|---|---|---|---|")
     for r in rows:
         print(f"| {r['config']} | {r['alu_lane_ops_per_px']:.1f} | {r['instr_per_px']:.1f} | {r['alu_floor_us']:.1f} | "
-              f"{r['hbm_floor_us']:.1f} | {r['kernel_us']:.1f} | {r['alu_frac']:.2f} | {r['hbm_frac']:.2f} |")
+              f"{r['issue_floor_us']:.1f} | {r['hbm_floor_us']:.1f} | {r['kernel_us']:.1f} | {r['alu_frac']:.2f} | "
+              f"{r['issue_frac']:.2f} | {r['hbm_frac']:.2f} |")
 
 
 if __name__ == "__main__":
