@@ -137,3 +137,51 @@ def test_gpu_strip_plan_matches_whole_frame(cuda_ok):
                 tot += c
             assert np.array_equal(np.concatenate(parts), whole), (world, passes)
             assert list(tot) == [st.minmax_scans, st.sorts, st.replacements, st.detected]
+
+
+def _cuda_worker(rank, world, port, case, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)  # both ranks share the one GPU here
+    try:
+        torch.cuda.set_device(0)
+        cfg, batch, k, method, passes, h, w = case
+        scene = CONFIGS[cfg].with_shape(frames=batch, height=h, width=w)
+        img = generate(scene, nframes=batch)
+        if batch == 1:
+            img = img[0]
+        out, stats = sharding.run_filter_distributed(img, k, method, passes)  # default: CUDA strips
+        q.put((rank, None if out is None else out.tobytes(), stats))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [("c4", 1, 11, "fnr", 2, 700, 640), ("c2", 6, 5, "fnr", 1, 256, 320),
+                                  ("c3", 1, 7, "mf", 1, 300, 512)])
+def test_gpu_world2_run_filter_distributed(cuda_ok, case):
+    """Two ranks (spawned processes, gloo control plane) filtering their row strips /
+    frame shards with the CUDA kernels reassemble exactly the single-process result."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cuda_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg, batch, k, method, passes, h, w = case
+    scene = CONFIGS[cfg].with_shape(frames=batch, height=h, width=w)
+    img = generate(scene, nframes=batch)
+    want, st = oracle.run_filter_c(img if batch > 1 else img[0], k, method, passes)
+    by_rank = {r: (o, s) for r, o, s in res}
+    assert by_rank[1][0] is None and by_rank[0][0] == want.tobytes()
+    s = by_rank[0][1]
+    assert [s["minmax_scans"], s["sorts"], s["replacements"], s["detected"], s["passes"]] == list(st.counters())
