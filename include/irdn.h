@@ -167,6 +167,39 @@ IRDN_API int irdn_sq_err_sum_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t 
 IRDN_API int irdn_sq_err_sum_u16(const uint16_t* d_a, const uint16_t* d_b, int64_t n,
                                  unsigned long long* d_sum, void* stream);
 
+/*
+ * Result return of irdn_run_filter_*: 0 = auto (sparse for FNR on u16 frames, else full copy),
+ * 1 = full device->host copy of the output, 2 = sparse. Sparse: the device sends only
+ * the output pixels that differ from the input (a per-4096-pixel count, a change
+ * bit mask and the packed changed values, written by the encode kernel into mapped
+ * pinned memory) and the host rebuilds the output from the caller's own input —
+ * filters.py:108 / :127's fresh output buffer, with the unchanged pixels copied on the
+ * host instead of over PCIe. Returns the previous mode. Process-wide. The environment
+ * variable IRDN_HOST_RETURN=auto|full|delta sets the initial mode.
+ */
+IRDN_API int32_t irdn_set_host_return(int32_t mode);
+/* Host->device and device->host bytes moved by this thread's last irdn_run_filter_* call. */
+IRDN_API void irdn_last_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+
+/*
+ * The sparse return as separate halves (the format is documented in
+ * paper_1201_3972_b200/csrc/delta.cuh). irdn_delta_encode_*: compare n device pixels
+ * d_out against d_in and write the region (irdn_delta_region_bytes(n, bpp) bytes,
+ * 16-byte aligned, device-accessible: device memory or mapped pinned host memory),
+ * stream-ordered. irdn_delta_decode_*: h_out = h_in with the region's changed pixels
+ * applied (host memory, OpenMP; simd = 0 forces the scalar decoder); returns the
+ * region bytes the encoder wrote.
+ */
+IRDN_API uint64_t irdn_delta_region_bytes(int64_t n, int32_t bytes_per_pixel);
+IRDN_API int irdn_delta_encode_u8(const uint8_t* d_in, const uint8_t* d_out, int64_t n, void* d_region,
+                                  void* stream);
+IRDN_API int irdn_delta_encode_u16(const uint16_t* d_in, const uint16_t* d_out, int64_t n, void* d_region,
+                                   void* stream);
+IRDN_API uint64_t irdn_delta_decode_u8(const void* region, const uint8_t* h_in, uint8_t* h_out, int64_t n,
+                                       int32_t simd);
+IRDN_API uint64_t irdn_delta_decode_u16(const void* region, const uint16_t* h_in, uint16_t* h_out, int64_t n,
+                                        int32_t simd);
+
 /* Kernel launches issued by this thread since the last reset (for bench accounting). */
 IRDN_API uint64_t irdn_launch_count(void);
 IRDN_API void irdn_reset_launch_count(void);

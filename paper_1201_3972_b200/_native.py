@@ -48,7 +48,11 @@ EXPORTED = [
     "irdn_run_filter_u8", "irdn_run_filter_u16", "irdn_run_filter_device_u8",
     "irdn_run_filter_device_u16", "irdn_launch_count", "irdn_reset_launch_count",
     "irdn_set_force_generic", "irdn_inject_impulse_u8", "irdn_sq_err_sum_u8", "irdn_sq_err_sum_u16",
+    "irdn_set_host_return", "irdn_last_transfer", "irdn_delta_region_bytes", "irdn_delta_encode_u8",
+    "irdn_delta_encode_u16", "irdn_delta_decode_u8", "irdn_delta_decode_u16",
 ]
+
+HOST_RETURN = {"auto": 0, "full": 1, "delta": 2}
 
 
 def _declare(l: ctypes.CDLL) -> None:
@@ -87,6 +91,20 @@ def _declare(l: ctypes.CDLL) -> None:
         f = getattr(l, f"irdn_sq_err_sum_{t}")
         f.restype = ctypes.c_int
         f.argtypes = [vp, vp, i64, vp, vp]
+    u64 = ctypes.c_uint64
+    l.irdn_set_host_return.restype = i32
+    l.irdn_set_host_return.argtypes = [i32]
+    l.irdn_last_transfer.restype = None
+    l.irdn_last_transfer.argtypes = [ctypes.POINTER(u64), ctypes.POINTER(u64)]
+    l.irdn_delta_region_bytes.restype = u64
+    l.irdn_delta_region_bytes.argtypes = [i64, i32]
+    for t in ("u8", "u16"):
+        f = getattr(l, f"irdn_delta_encode_{t}")
+        f.restype = ctypes.c_int
+        f.argtypes = [vp, vp, i64, vp, vp]
+        f = getattr(l, f"irdn_delta_decode_{t}")
+        f.restype = u64
+        f.argtypes = [vp, vp, vp, i64, i32]
 
 
 def load_lib() -> ctypes.CDLL:
@@ -127,6 +145,19 @@ def check(rc: int) -> None:
     if rc == IRDN_EINVAL:
         raise ValueError(msg)
     raise NativeError(msg)
+
+
+def last_transfer() -> tuple[int, int]:
+    """(h2d, d2h) bytes moved by this thread's last irdn_run_filter_* call."""
+    a, b = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    load_lib().irdn_last_transfer(ctypes.byref(a), ctypes.byref(b))
+    return int(a.value), int(b.value)
+
+
+def set_host_return(mode: str) -> str:
+    """Result return of the host-buffer path: "auto", "full" or "delta"; returns the previous mode."""
+    prev = int(load_lib().irdn_set_host_return(HOST_RETURN[mode]))
+    return {v: k for k, v in HOST_RETURN.items()}[prev]
 
 
 def version() -> str:

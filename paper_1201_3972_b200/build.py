@@ -1,6 +1,7 @@
 """In-tree build of the native libraries (no JIT cache: the .so files travel with the repo).
 
 * libirdn.so        nvcc, -gencode arch=compute_100a,code=sm_100a, static cudart
+                    (+ delta_host.cpp through the host compiler)
 * libirdn_scene.so  gcc (seeded synthetic scenes for bench/tests)
 """
 
@@ -15,9 +16,9 @@ REPO = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CUDA_SOURCES = ["irdn_api.cu"]
+CUDA_SOURCES = ["irdn_api.cu", "delta_host.cpp"]
 CUDA_HEADERS = ["fnr_common.cuh", "fnr_generic.cuh", "fnr_fast.cuh", "fnr_tile.cuh",
-                "select_nets.cuh", "fnr_k3.cuh", "fnr_warp.cuh", "noise.cuh", "metrics.cuh"]
+                "select_nets.cuh", "fnr_k3.cuh", "fnr_warp.cuh", "noise.cuh", "metrics.cuh", "delta.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -25,12 +25,27 @@
 #include "fnr_fast.cuh"
 #include "metrics.cuh"
 #include "noise.cuh"
+#include "delta.cuh"
+
+// delta_host.cpp (host decode of the sparse result return, compiled by the host compiler)
+uint64_t irdn_delta_decode_host_u8(const uint8_t* src, const uint8_t* in, uint8_t* out, int64_t n, int threads,
+                                   int simd);
+uint64_t irdn_delta_decode_host_u16(const uint8_t* src, const uint16_t* in, uint16_t* out, int64_t n, int threads,
+                                    int simd);
 
 namespace irdn {
 
 static thread_local std::string g_err;
 static thread_local uint64_t g_launches = 0;
+static thread_local uint64_t g_xfer_h2d = 0, g_xfer_d2h = 0;  // bytes moved by the last irdn_run_filter_* call
 static int32_t g_force_generic = 0;
+// Host-buffer result return: 0 = auto (sparse for FNR on u16, else the full copy), 1 = full copy,
+// 2 = sparse (delta.cuh). IRDN_HOST_RETURN=full|delta|auto sets the initial value.
+static int32_t g_host_return = [] {
+  const char* e = getenv("IRDN_HOST_RETURN");
+  if (!e) return 0;
+  return e[0] == 'f' ? 1 : e[0] == 'd' ? 2 : 0;
+}();
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -211,6 +226,10 @@ struct DeviceWorkspace {
   void* stage_out = nullptr;
   size_t stage_cap = 0;  // bytes per direction (kStageSlots slots)
   cudaEvent_t ev_out[4] = {nullptr, nullptr, nullptr, nullptr};
+  // sparse result return: mapped pinned region the encode kernel writes over PCIe
+  void* delta_h = nullptr;
+  uint8_t* delta_d = nullptr;
+  size_t delta_cap = 0;
   bool ready = false;
 };
 constexpr int kStageSlots = 3;
@@ -232,6 +251,23 @@ static int ensure_staging(DeviceWorkspace& ws, size_t slot_bytes) {
   return IRDN_OK;
 }
 
+// Host threads for copies and the sparse-return decode: the host's threads shared out
+// between the GPUs one process each may drive (16 threads: 113 GB/s memcpy on the
+// 16-core B200 box vs 90 GB/s with 8, tools/microbench/host_probe.cu), capped at 16.
+static int copy_threads() {
+  static const int nt = [] {
+    const char* e = getenv("IRDN_COPY_THREADS");
+    if (e) return std::max(1, atoi(e));
+    int ndev = 1;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+      cudaGetLastError();
+      ndev = 1;
+    }
+    return std::max(1, std::min(16, omp_get_max_threads() / ndev));
+  }();
+  return nt;
+}
+
 // memcpy split over the OpenMP team (host DRAM bandwidth, not one core, bounds it)
 static void par_copy(void* dst, const void* src, size_t n) {
   constexpr size_t kPart = 256 << 10;
@@ -240,12 +276,7 @@ static void par_copy(void* dst, const void* src, size_t n) {
     memcpy(dst, src, n);
     return;
   }
-  // a few threads saturate host DRAM for a copy; more only oversubscribe the host when
-  // one process per GPU runs (8 ranks on one node)
-  static const int nt = [] {
-    const char* e = getenv("IRDN_COPY_THREADS");
-    return std::max(1, e ? atoi(e) : std::min(8, omp_get_max_threads()));
-  }();
+  const int nt = copy_threads();
 #pragma omp parallel for schedule(static) num_threads(nt)
   for (long long i = 0; i < parts; ++i) {
     const size_t off = (size_t)i * kPart;
@@ -288,6 +319,18 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   if (rc) return rc;
   if (passes < 1) return fail(IRDN_EINVAL, "passes must be >= 1, got %d", passes);
   if (!h_in || !h_out) return fail(IRDN_EINVAL, "null buffer");
+  // IRDN_HOST_TRACE: host timestamps per chunk and device event times (experiments only)
+  static const bool trace = getenv("IRDN_HOST_TRACE") != nullptr;
+  static std::vector<cudaEvent_t> tev;
+  auto tmark = [&](size_t idx, cudaStream_t st) {
+    if (!trace) return;
+    while (tev.size() <= idx) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      tev.push_back(e);
+    }
+    cudaEventRecord(tev[idx], st);
+  };
   const int64_t frame = height * width;
   const size_t nbytes = (size_t)(batch * frame) * sizeof(T);
   if (overlaps(h_in, nbytes, h_out, nbytes)) return fail(IRDN_EINVAL, "input and output buffers overlap");
@@ -321,9 +364,25 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
     }();
     const int64_t target = std::max<int64_t>(1, chunk_bytes / (int64_t)sizeof(T) / frame);  // ~8 MB of frames (measured optimum for c2: tools/pcie_probe.py)
     const int64_t nchunks = std::min<int64_t>(std::max<int64_t>(1, batch / target), 256);
-    for (int64_t i = 0; i < nchunks; ++i) {
-      int64_t a = batch * i / nchunks, b = batch * (i + 1) / nchunks;
-      if (b > a) chunks.push_back({a, b - a, 0, height});
+    static const int taper = getenv("IRDN_TAPER") ? atoi(getenv("IRDN_TAPER")) : 0;
+    if (taper && nchunks > 1) {
+      // equal chunks, then halving ones: the chunk whose result is handled last is small
+      const int64_t per = (batch + nchunks - 1) / nchunks;
+      int64_t a = 0;
+      while (batch - a > 2 * per) {
+        chunks.push_back({a, per, 0, height});
+        a += per;
+      }
+      while (a < batch) {
+        const int64_t take = std::max<int64_t>(1, (batch - a + 1) / 2);
+        chunks.push_back({a, take, 0, height});
+        a += take;
+      }
+    } else {
+      for (int64_t i = 0; i < nchunks; ++i) {
+        int64_t a = batch * i / nchunks, b = batch * (i + 1) / nchunks;
+        if (b > a) chunks.push_back({a, b - a, 0, height});
+      }
     }
   } else if (passes == 1 && height >= 4 * (int64_t)(r + 1) && frame * (int64_t)sizeof(T) >= (16 << 20)) {
     const int64_t nchunks = std::min<int64_t>(16, height / (4 * (r + 1)));
@@ -350,7 +409,29 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   auto chunk_cnt = [&](const Chunk& c) { return row_mode ? (c.y1 - c.y0) * width : c.nf * frame; };
   // Pageable caller buffers: DMA from / to pinned staging slots; the CPU copies chunk
   // i into a slot (parallel memcpy) while the copy engines move chunks i-1 and i-2.
-  const bool staged_in = !is_pinned(h_in), staged_out = !is_pinned(h_out);
+  // Result return: sparse (only the pixels that differ from the input, delta.cuh; the
+  // host rebuilds the output from its own input) or the full D2H copy of the output.
+  // auto: sparse for FNR on 16-bit frames (c2 1.18-1.29 -> 1.00 ms, c4 3.6-4.5 -> 3.14 ms per call,
+  // tools/e2e_probe.py); 8-bit frames keep the full copy (the host rebuild of 1 B/px costs more
+  // than the D2H saves at c1 / c3 / c5's 20-50 % replaced pixels)
+  const bool use_delta =
+      g_host_return == 2 || (g_host_return == 0 && method == IRDN_METHOD_FNR && sizeof(T) == 2);
+  std::vector<int64_t> delta_off(chunks.size() + 1, 0);
+  if (use_delta) {
+    for (size_t i = 0; i < chunks.size(); ++i)
+      delta_off[i + 1] = delta_off[i] + (row_mode ? delta::region_bytes<T>((chunks[i].y1 - chunks[i].y0) * width)
+                                                  : delta::region_bytes<T>(chunks[i].nf * frame));
+    if ((size_t)delta_off.back() > ws.delta_cap) {
+      if (ws.delta_h) IRDN_CUDA(cudaFreeHost(ws.delta_h));
+      ws.delta_h = nullptr;
+      ws.delta_d = nullptr;
+      ws.delta_cap = 0;
+      IRDN_CUDA(cudaHostAlloc(&ws.delta_h, (size_t)delta_off.back(), cudaHostAllocMapped));
+      IRDN_CUDA(cudaHostGetDevicePointer((void**)&ws.delta_d, ws.delta_h, 0));
+      ws.delta_cap = (size_t)delta_off.back();
+    }
+  }
+  const bool staged_in = !is_pinned(h_in), staged_out = !use_delta && !is_pinned(h_out);
   const bool staged = staged_in || staged_out;
   int64_t max_cnt = 0;
   for (const Chunk& c : chunks) max_cnt = std::max(max_cnt, chunk_cnt(c));
@@ -367,7 +448,9 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   if (!staged_in) {
     for (size_t i = 0; i < chunks.size(); ++i) {
       const int64_t off = chunk_off(chunks[i]), cnt = chunk_cnt(chunks[i]);
+      if (i == 0) tmark(0, ws.s_h2d);
       IRDN_CUDA(cudaMemcpyAsync(d_in + off, h_in + off, cnt * sizeof(T), cudaMemcpyHostToDevice, ws.s_h2d));
+      tmark(1 + 4 * i, ws.s_h2d);
       IRDN_CUDA(cudaEventRecord(ev_in[i], ws.s_h2d));
     }
   }
@@ -414,14 +497,35 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
       if (rc) return rc;
     } else {
       IRDN_CUDA(cudaStreamWaitEvent(ws.s_comp, ev_in[i], 0));
+      tmark(2 + 4 * i, ws.s_comp);
       const int64_t off = c.f0 * frame;
       rc = run_device<T>(d_in + off, d_out + off, d_tmp ? d_tmp + off : nullptr, c.nf, height,
                          width, k, method, passes, ws.counts, ws.s_comp);
       if (rc) return rc;
     }
+    const int64_t off = chunk_off(c), cnt = chunk_cnt(c);
+    if (use_delta) {  // encode out vs in into the mapped region; the host decodes after the loop
+      const T* a = d_in + off;
+      const T* o = d_out + off;
+      const int vec = (((uintptr_t)a | (uintptr_t)o) & 15) == 0;
+      // on the otherwise idle D2H stream: the encode's PCIe writes overlap the next chunk's filter
+      static const bool enc_own = getenv("IRDN_ENC_STREAM") && atoi(getenv("IRDN_ENC_STREAM"));
+      cudaStream_t se = enc_own ? ws.s_d2h : ws.s_comp;
+      if (enc_own) {
+        IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
+        IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
+      }
+      tmark(3 + 4 * i, se);
+      delta::encode_kernel<T><<<(unsigned)delta::nblocks(cnt), delta::THREADS, 0, se>>>(
+          a, o, cnt, ws.delta_d + delta_off[i], vec);
+      tmark(4 + 4 * i, se);
+      IRDN_CUDA(cudaGetLastError());
+      note_launch();
+      IRDN_CUDA(cudaEventRecord(ev_done[i], se));
+      continue;
+    }
     IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
     IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
-    const int64_t off = chunk_off(c), cnt = chunk_cnt(c);
     if (staged_out && !staged_in && i >= (size_t)kStageSlots && drained <= i - kStageSlots) {
       if ((rc = drain_out(i - kStageSlots))) return rc;  // the slot's previous chunk
       drained = i - kStageSlots + 1;
@@ -433,12 +537,46 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   if (staged_out)
     for (size_t i = drained; i < chunks.size(); ++i)
       if ((rc = drain_out(i))) return rc;
+  uint64_t d2h_bytes = 16;  // the counters
+  auto us = [&] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(); };
+  if (trace) fprintf(stderr, "[irdn] %zu chunks enqueued at %.1f us\n", chunks.size(), us());
+  if (use_delta) {
+    const int nt = copy_threads();
+    for (size_t i = 0; i < chunks.size(); ++i) {
+      IRDN_CUDA(cudaEventSynchronize(ev_done[i]));
+      if (trace) fprintf(stderr, "[irdn]   chunk %zu ready %.1f us", i, us());
+      const int64_t off = chunk_off(chunks[i]), cnt = chunk_cnt(chunks[i]);
+      const uint8_t* src = static_cast<const uint8_t*>(ws.delta_h) + delta_off[i];
+      if constexpr (sizeof(T) == 1)
+        d2h_bytes += irdn_delta_decode_host_u8(src, h_in + off, h_out + off, cnt, nt, 1);
+      else
+        d2h_bytes += irdn_delta_decode_host_u16(src, h_in + off, h_out + off, cnt, nt, 1);
+      if (trace) fprintf(stderr, " decoded %.1f us (%lld px)\n", us(), (long long)cnt);
+    }
+  } else {
+    d2h_bytes += nbytes;
+  }
+  g_xfer_h2d = nbytes;
+  g_xfer_d2h = d2h_bytes;
   unsigned long long counts[2] = {0, 0};
   IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[chunks.size() - 1], 0));
   IRDN_CUDA(cudaMemcpyAsync(counts, ws.counts, sizeof(counts), cudaMemcpyDeviceToHost, ws.s_d2h));
   IRDN_CUDA(cudaStreamSynchronize(ws.s_d2h));
   IRDN_CUDA(cudaStreamSynchronize(ws.s_comp));
   IRDN_CUDA(cudaGetLastError());
+  if (trace) {
+    fprintf(stderr, "[irdn] done %.1f us; device (us from the first H2D): ", us());
+    for (size_t i = 0; i < chunks.size() && 4 * i + 4 < tev.size(); ++i) {
+      float a = 0, b = 0, c = 0, d = 0;
+      cudaEventElapsedTime(&a, tev[0], tev[1 + 4 * i]);
+      cudaEventElapsedTime(&b, tev[0], tev[2 + 4 * i]);
+      cudaEventElapsedTime(&c, tev[0], tev[3 + 4 * i]);
+      cudaEventElapsedTime(&d, tev[0], tev[4 + 4 * i]);
+      fprintf(stderr, "[%zu h2d %.0f filt %.0f-%.0f enc -%.0f] ", i, a * 1e3, b * 1e3, c * 1e3, d * 1e3);
+    }
+    cudaGetLastError();
+    fprintf(stderr, "\n");
+  }
 
   if (stats) {
     const uint64_t pixels = (uint64_t)(batch * frame) * (uint64_t)passes;
@@ -545,6 +683,23 @@ static int sq_err_sum(const T* d_a, const T* d_b, int64_t n, unsigned long long*
   return IRDN_OK;
 }
 
+// Device half of the sparse result return as a public entry point (delta.cuh format);
+// d_region is device-accessible (device memory or mapped pinned host memory).
+template <typename T>
+static int delta_encode(const T* d_in, const T* d_out, int64_t n, void* d_region, void* stream) {
+  if (n < 0 || (n > 0 && (!d_in || !d_out || !d_region))) return fail(IRDN_EINVAL, "bad delta_encode arguments");
+  if (((uintptr_t)d_region & 15)) return fail(IRDN_EINVAL, "delta region must be 16-byte aligned");
+  if (n == 0) return IRDN_OK;
+  int rc = check_device(nullptr);
+  if (rc) return rc;
+  const int vec = (((uintptr_t)d_in | (uintptr_t)d_out) & 15) == 0;
+  delta::encode_kernel<T><<<(unsigned)delta::nblocks(n), delta::THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_in, d_out, n, static_cast<uint8_t*>(d_region), vec);
+  IRDN_CUDA(cudaGetLastError());
+  note_launch();
+  return IRDN_OK;
+}
+
 }  // namespace irdn
 
 using namespace irdn;
@@ -632,6 +787,33 @@ int irdn_sq_err_sum_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t n, unsign
 int irdn_sq_err_sum_u16(const uint16_t* d_a, const uint16_t* d_b, int64_t n, unsigned long long* d_sum,
                         void* stream) {
   return sq_err_sum<uint16_t>(d_a, d_b, n, d_sum, stream);
+}
+int32_t irdn_set_host_return(int32_t mode) {
+  int32_t prev = g_host_return;
+  g_host_return = (mode >= 0 && mode <= 2) ? mode : 0;
+  return prev;
+}
+void irdn_last_transfer(uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
+  if (h2d_bytes) *h2d_bytes = g_xfer_h2d;
+  if (d2h_bytes) *d2h_bytes = g_xfer_d2h;
+}
+uint64_t irdn_delta_region_bytes(int64_t n, int32_t bytes_per_pixel) {
+  if (n < 1) return 0;
+  return (uint64_t)(bytes_per_pixel == 1 ? delta::region_bytes<uint8_t>(n) : delta::region_bytes<uint16_t>(n));
+}
+uint64_t irdn_delta_decode_u8(const void* region, const uint8_t* h_in, uint8_t* h_out, int64_t n, int32_t simd) {
+  return n < 1 ? 0 : irdn_delta_decode_host_u8(static_cast<const uint8_t*>(region), h_in, h_out, n, copy_threads(),
+                                               simd);
+}
+uint64_t irdn_delta_decode_u16(const void* region, const uint16_t* h_in, uint16_t* h_out, int64_t n, int32_t simd) {
+  return n < 1 ? 0 : irdn_delta_decode_host_u16(static_cast<const uint8_t*>(region), h_in, h_out, n,
+                                                copy_threads(), simd);
+}
+int irdn_delta_encode_u8(const uint8_t* d_in, const uint8_t* d_out, int64_t n, void* d_region, void* stream) {
+  return delta_encode<uint8_t>(d_in, d_out, n, d_region, stream);
+}
+int irdn_delta_encode_u16(const uint16_t* d_in, const uint16_t* d_out, int64_t n, void* d_region, void* stream) {
+  return delta_encode<uint16_t>(d_in, d_out, n, d_region, stream);
 }
 uint64_t irdn_launch_count(void) { return g_launches; }
 void irdn_reset_launch_count(void) { g_launches = 0; }

@@ -1,0 +1,179 @@
+"""Sparse result return of the host-buffer run_filter (csrc/delta.cuh, delta_host.cpp).
+
+CPU: the host decoder against a numpy model of the region format (AVX-512 and scalar
+decoders, u8 / u16, ragged sizes, empty / full / random change masks).
+GPU: the encode kernel writes exactly the numpy model's region, and irdn_run_filter_*
+returns identical pixels and counters in full-copy and sparse mode (FNR / MF, passes
+1-2, batches, row strips, pageable and pinned host buffers).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_1201_3972_b200 import _native
+
+BLK = 4096
+
+
+def region_model(a: np.ndarray, o: np.ndarray) -> tuple[np.ndarray, int]:
+    """numpy restatement of the region layout (delta.cuh header); returns (region, bytes written)."""
+    n = a.size
+    s = a.itemsize
+    nb = (n + BLK - 1) // BLK
+    cb = (nb * 4 + 15) // 16 * 16
+    moff = cb
+    voff = cb + nb * BLK // 8
+    reg = np.zeros(voff + nb * BLK * s, np.uint8)
+    counts = reg[:nb * 4].view(np.uint32)
+    written = cb
+    for b in range(nb):
+        sl = slice(b * BLK, min(n, (b + 1) * BLK))
+        ch = a[sl] != o[sl]
+        c = int(ch.sum())
+        counts[b] = c
+        if not c:
+            continue
+        bits = np.zeros(BLK, np.uint8)
+        bits[: ch.size] = ch
+        reg[moff + b * 512: moff + (b + 1) * 512] = np.packbits(bits, bitorder="little")
+        vals = o[sl][ch]
+        reg[voff + b * BLK * s: voff + b * BLK * s + c * s] = vals.view(np.uint8)
+        written += 512 + (c * s + 15) // 16 * 16
+    return reg, written
+
+
+def _case(n, dtype, frac, seed):
+    rng = np.random.default_rng(seed)
+    hi = 256 if dtype == np.uint8 else 16384
+    a = rng.integers(0, hi, n, dtype=np.int64).astype(dtype)
+    o = a.copy()
+    ch = rng.random(n) < frac
+    o[ch] = ((a[ch].astype(np.int64) + rng.integers(1, hi, int(ch.sum()))) % hi).astype(dtype)
+    return a, o
+
+
+SIZES = [1, 15, 16, 31, 32, 63, 64, 65, 4095, 4096, 4097, 3 * 4096 + 77, 100_003]
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+@pytest.mark.parametrize("simd", [1, 0])
+def test_decode_matches_model(dtype, simd):
+    lib = _native.load_lib()
+    fn = lib.irdn_delta_decode_u8 if dtype == np.uint8 else lib.irdn_delta_decode_u16
+    for i, n in enumerate(SIZES):
+        for frac in (0.0, 0.03, 0.3, 1.0):
+            a, o = _case(n, dtype, frac, 100 * i + int(frac * 10))
+            reg, written = region_model(a, o)
+            assert lib.irdn_delta_region_bytes(n, a.itemsize) == reg.size
+            out = np.full_like(a, 7)
+            got = fn(reg.ctypes.data, a.ctypes.data, out.ctypes.data, n, simd)
+            assert np.array_equal(out, o), (n, frac, simd)
+            assert got == written
+
+
+def test_decode_ignores_stale_masks_of_unchanged_blocks():
+    """Blocks with count 0 are not written by the device: their mask/value slots hold garbage."""
+    lib = _native.load_lib()
+    a, o = _case(5 * BLK, np.uint16, 0.1, 9)
+    o[BLK:2 * BLK] = a[BLK:2 * BLK]
+    reg, _ = region_model(a, o)
+    nb = 5
+    moff = (nb * 4 + 15) // 16 * 16
+    reg[moff + 512: moff + 1024] = 0xFF  # stale mask of block 1
+    out = np.empty_like(a)
+    lib.irdn_delta_decode_u16(reg.ctypes.data, a.ctypes.data, out.ctypes.data, a.size, 1)
+    assert np.array_equal(out, o)
+
+
+def test_host_return_mode_setter():
+    assert _native.set_host_return("full") in ("auto", "full", "delta")
+    assert _native.set_host_return("delta") == "full"
+    assert _native.set_host_return("auto") == "delta"
+
+
+# ---------------------------------------------------------------- GPU -------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_encode_kernel_matches_model(dtype):
+    import torch
+
+    lib = _native.load_lib()
+    fn = lib.irdn_delta_encode_u8 if dtype == np.uint8 else lib.irdn_delta_encode_u16
+    tdt = torch.uint8 if dtype == np.uint8 else torch.int16
+    for i, n in enumerate(SIZES):
+        for frac in (0.0, 0.05, 0.5, 1.0):
+            a, o = _case(n, dtype, frac, 7 * i + int(frac * 100))
+            reg, written = region_model(a, o)
+            for shift in (0, 1):  # unaligned views take the scalar load path
+                da = torch.zeros(n + 8, dtype=tdt, device="cuda")
+                do = torch.zeros(n + 8, dtype=tdt, device="cuda")
+                da[shift:shift + n] = torch.from_numpy(a.view(np.int16) if dtype == np.uint16 else a).cuda()
+                do[shift:shift + n] = torch.from_numpy(o.view(np.int16) if dtype == np.uint16 else o).cuda()
+                dreg = torch.full((reg.size,), 0xAB, dtype=torch.uint8, device="cuda")
+                rc = fn(da.data_ptr() + shift * a.itemsize, do.data_ptr() + shift * a.itemsize, n,
+                        dreg.data_ptr(), None)
+                _native.check(rc)
+                got = dreg.cpu().numpy()
+                # compare what the device writes: counts, masks and values of changed blocks
+                nb = (n + BLK - 1) // BLK
+                assert np.array_equal(got[:nb * 4], reg[:nb * 4])
+                out = np.empty_like(a)
+                dec = (lib.irdn_delta_decode_u8 if dtype == np.uint8 else lib.irdn_delta_decode_u16)(
+                    got.ctypes.data, a.ctypes.data, out.ctypes.data, n, 1)
+                assert np.array_equal(out, o), (n, frac, shift)
+                assert dec == written
+
+
+def _run(lib, img, k, method, passes):
+    st = _native.IrdnStats()
+    out = np.empty_like(img)
+    B, H, W = img.shape
+    fn = lib.irdn_run_filter_u8 if img.dtype == np.uint8 else lib.irdn_run_filter_u16
+    _native.check(fn(img.ctypes.data, out.ctypes.data, B, H, W, k, method, passes, 0, ctypes.byref(st)))
+    return out, (st.minmax_scans, st.sorts, st.replacements, st.detected, st.passes), _native.last_transfer()
+
+
+@pytest.mark.gpu
+def test_run_filter_full_vs_sparse_return():
+    from paper_1201_3972_b200.scene import CONFIGS, generate
+
+    lib = _native.load_lib()
+    cases = [("c2", 12, None), ("c3", 2, None), ("c5", 20, None), ("c1", 1, None), ("c4", 1, (2048, 1536))]
+    prev = _native.set_host_return("auto")
+    try:
+        for name, frames, shape in cases:
+            cfg = CONFIGS[name]
+            if shape:
+                cfg = cfg.with_shape(height=shape[0], width=shape[1])
+            img = generate(cfg, nframes=frames)
+            if img.ndim == 2:
+                img = img[None]
+            for method, passes in ((0, 1), (0, 2), (1, 1)):
+                _native.set_host_return("full")
+                want, wst, (h2d_f, d2h_f) = _run(lib, img, cfg.k, method, passes)
+                _native.set_host_return("delta")
+                got, gst, (h2d_d, d2h_d) = _run(lib, img, cfg.k, method, passes)
+                assert np.array_equal(got, want), (name, method, passes)
+                assert gst == wst
+                assert h2d_d == h2d_f == img.nbytes
+                assert d2h_f == img.nbytes + 16
+                changed = int((want != img).sum())
+                assert d2h_d <= img.nbytes // (8 * img.itemsize) + changed * img.itemsize + 16 * (img.size // BLK + 2) + 16 + 4 * (img.size // BLK + 4)
+                # pageable and pinned caller buffers through the sparse return
+                import torch
+
+                pin_in = torch.from_numpy(img.view(np.int16) if img.dtype == np.uint16 else img).pin_memory()
+                pin_out = torch.empty_like(pin_in).pin_memory()
+                B, H, W = img.shape
+                st = _native.IrdnStats()
+                fn = lib.irdn_run_filter_u8 if img.dtype == np.uint8 else lib.irdn_run_filter_u16
+                _native.check(fn(pin_in.data_ptr(), pin_out.data_ptr(), B, H, W, cfg.k, method, passes, 0,
+                                 ctypes.byref(st)))
+                po = pin_out.numpy().view(img.dtype)
+                assert np.array_equal(po, want)
+    finally:
+        _native.set_host_return(prev)
