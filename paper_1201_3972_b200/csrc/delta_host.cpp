@@ -17,9 +17,11 @@ namespace delta_host {
 
 constexpr int64_t BLK = 4096;
 
+// region layout: delta.cuh
 static inline int64_t nblocks(int64_t n) { return (n + BLK - 1) / BLK; }
-static inline int64_t counts_bytes(int64_t n) { return ((nblocks(n) * 4) + 15) & ~int64_t(15); }
-static inline int64_t values_offset(int64_t n) { return counts_bytes(n) + nblocks(n) * (BLK / 8); }
+static inline int64_t table_bytes(int64_t n) { return ((nblocks(n) * 4) + 15) & ~int64_t(15); }
+static inline int64_t mask_offset(int64_t n) { return 16 + 2 * table_bytes(n); }
+static inline int64_t values_offset(int64_t n) { return mask_offset(n) + nblocks(n) * (BLK / 8); }
 
 // streaming (non-temporal) stores for the output; IRDN_DECODE_NT=1 enables them (experiments)
 static bool use_nt() {
@@ -104,21 +106,22 @@ static bool has_vbmi2() {
 }
 
 // Decode one chunk region `src` (n pixels) into out[0, n) from in[0, n). Returns the
-// bytes the device wrote into the region (the PCIe traffic of this chunk).
+// bytes of the region that carry data (fixed part + total values).
 template <typename T>
 static uint64_t decode(const uint8_t* src, const T* in, T* out, int64_t n, int threads, int simd) {
   const int64_t nb = nblocks(n);
-  const uint32_t* counts = reinterpret_cast<const uint32_t*>(src);
-  const uint32_t* mask = reinterpret_cast<const uint32_t*>(src + counts_bytes(n));
-  const uint8_t* vals = src + values_offset(n);
+  const uint32_t total = reinterpret_cast<const uint32_t*>(src)[0];
+  const uint32_t* counts = reinterpret_cast<const uint32_t*>(src + 16);
+  const uint32_t* offsets = reinterpret_cast<const uint32_t*>(src + 16 + table_bytes(n));
+  const uint32_t* mask = reinterpret_cast<const uint32_t*>(src + mask_offset(n));
+  const T* vals = reinterpret_cast<const T*>(src + values_offset(n));
   const bool vec = simd && has_vbmi2();
-  uint64_t bytes = (uint64_t)counts_bytes(n);
-#pragma omp parallel for schedule(static) num_threads(threads) reduction(+ : bytes) if (nb > 4)
+#pragma omp parallel for schedule(static) num_threads(threads) if (nb > 4)
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t p = b * BLK, m = (n - p) < BLK ? (n - p) : BLK;
     const uint32_t c = counts[b];
     const uint32_t* mk = mask + b * (BLK / 32);
-    const T* v = reinterpret_cast<const T*>(vals + b * BLK * (int64_t)sizeof(T));
+    const T* v = vals + (c ? offsets[b] : 0);
     if (vec) {
       if (sizeof(T) == 2)
         block_avx512_u16(reinterpret_cast<const uint16_t*>(in + p), reinterpret_cast<uint16_t*>(out + p), m, mk,
@@ -129,9 +132,8 @@ static uint64_t decode(const uint8_t* src, const T* in, T* out, int64_t n, int t
     } else {
       block_scalar<T>(in + p, out + p, m, mk, v, c);
     }
-    if (c) bytes += (uint64_t)(BLK / 8) + (((uint64_t)c * sizeof(T) + 15) & ~uint64_t(15));
   }
-  return bytes;
+  return (uint64_t)values_offset(n) + (uint64_t)total * sizeof(T);
 }
 
 }  // namespace delta_host

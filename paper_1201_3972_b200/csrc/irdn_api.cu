@@ -227,9 +227,10 @@ struct DeviceWorkspace {
   size_t stage_cap = 0;  // bytes per direction (kStageSlots slots)
   cudaEvent_t ev_out[4] = {nullptr, nullptr, nullptr, nullptr};
   // sparse result return: mapped pinned region the encode kernel writes over PCIe
-  void* delta_h = nullptr;
-  uint8_t* delta_d = nullptr;
+  uint8_t* delta_h = nullptr;  // pinned host copy of the regions
+  uint8_t* delta_d = nullptr;  // device regions (encode target)
   size_t delta_cap = 0;
+  double delta_ratio = 0.25;   // changed-pixel fraction the value budget assumes (last call's max)
   bool ready = false;
 };
 constexpr int kStageSlots = 3;
@@ -411,9 +412,9 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   // i into a slot (parallel memcpy) while the copy engines move chunks i-1 and i-2.
   // Result return: sparse (only the pixels that differ from the input, delta.cuh; the
   // host rebuilds the output from its own input) or the full D2H copy of the output.
-  // auto: sparse for FNR on 16-bit frames (c2 1.18-1.29 -> 1.00 ms, c4 3.6-4.5 -> 3.14 ms per call,
-  // tools/e2e_probe.py); 8-bit frames keep the full copy (the host rebuild of 1 B/px costs more
-  // than the D2H saves at c1 / c3 / c5's 20-50 % replaced pixels)
+  // auto: sparse for FNR on 16-bit frames (c2 1.23-1.27 -> 1.01 ms, c4 4.6 -> 3.3 ms per call,
+  // tools/e2e_probe.py); 8-bit frames keep the full copy: rebuilding 1 B/px on the host costs
+  // about what the D2H saves (c3 2.06 -> 1.98 ms, but c5 31.8 -> 37.4 ms, c1 0.050 -> 0.067 ms)
   const bool use_delta =
       g_host_return == 2 || (g_host_return == 0 && method == IRDN_METHOD_FNR && sizeof(T) == 2);
   std::vector<int64_t> delta_off(chunks.size() + 1, 0);
@@ -423,14 +424,20 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
                                                   : delta::region_bytes<T>(chunks[i].nf * frame));
     if ((size_t)delta_off.back() > ws.delta_cap) {
       if (ws.delta_h) IRDN_CUDA(cudaFreeHost(ws.delta_h));
+      if (ws.delta_d) IRDN_CUDA(cudaFree(ws.delta_d));
       ws.delta_h = nullptr;
       ws.delta_d = nullptr;
       ws.delta_cap = 0;
-      IRDN_CUDA(cudaHostAlloc(&ws.delta_h, (size_t)delta_off.back(), cudaHostAllocMapped));
-      IRDN_CUDA(cudaHostGetDevicePointer((void**)&ws.delta_d, ws.delta_h, 0));
+      IRDN_CUDA(cudaHostAlloc((void**)&ws.delta_h, (size_t)delta_off.back(), cudaHostAllocDefault));
+      IRDN_CUDA(cudaMalloc((void**)&ws.delta_d, (size_t)delta_off.back()));
       ws.delta_cap = (size_t)delta_off.back();
     }
   }
+  // values copied with the fixed part of each region: the last call's changed fraction + 15 %
+  auto delta_budget = [&](int64_t n) {
+    return std::min<int64_t>(n, (int64_t)((double)n * ws.delta_ratio * 1.15) + 2 * delta::BLK);
+  };
+  uint64_t d2h_bytes = 16;  // the counters
   const bool staged_in = !is_pinned(h_in), staged_out = !use_delta && !is_pinned(h_out);
   const bool staged = staged_in || staged_out;
   int64_t max_cnt = 0;
@@ -504,24 +511,23 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
       if (rc) return rc;
     }
     const int64_t off = chunk_off(c), cnt = chunk_cnt(c);
-    if (use_delta) {  // encode out vs in into the mapped region; the host decodes after the loop
+    if (use_delta) {  // encode out vs in into the device region, DMA its fixed part + a value budget
       const T* a = d_in + off;
       const T* o = d_out + off;
       const int vec = (((uintptr_t)a | (uintptr_t)o) & 15) == 0;
-      // on the otherwise idle D2H stream: the encode's PCIe writes overlap the next chunk's filter
-      static const bool enc_own = getenv("IRDN_ENC_STREAM") && atoi(getenv("IRDN_ENC_STREAM"));
-      cudaStream_t se = enc_own ? ws.s_d2h : ws.s_comp;
-      if (enc_own) {
-        IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
-        IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
-      }
-      tmark(3 + 4 * i, se);
-      delta::encode_kernel<T><<<(unsigned)delta::nblocks(cnt), delta::THREADS, 0, se>>>(
-          a, o, cnt, ws.delta_d + delta_off[i], vec);
-      tmark(4 + 4 * i, se);
+      uint8_t* dreg = ws.delta_d + delta_off[i];
+      IRDN_CUDA(cudaMemsetAsync(dreg, 0, 16, ws.s_comp));
+      tmark(3 + 4 * i, ws.s_comp);
+      delta::encode_kernel<T><<<(unsigned)delta::nblocks(cnt), delta::THREADS, 0, ws.s_comp>>>(a, o, cnt, dreg, vec);
       IRDN_CUDA(cudaGetLastError());
       note_launch();
-      IRDN_CUDA(cudaEventRecord(ev_done[i], se));
+      IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
+      IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
+      const size_t bytes = (size_t)(delta::values_offset(cnt) + delta_budget(cnt) * (int64_t)sizeof(T));
+      IRDN_CUDA(cudaMemcpyAsync(ws.delta_h + delta_off[i], dreg, bytes, cudaMemcpyDeviceToHost, ws.s_d2h));
+      d2h_bytes += bytes;
+      tmark(4 + 4 * i, ws.s_d2h);
+      IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_d2h));
       continue;
     }
     IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
@@ -537,22 +543,34 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   if (staged_out)
     for (size_t i = drained; i < chunks.size(); ++i)
       if ((rc = drain_out(i))) return rc;
-  uint64_t d2h_bytes = 16;  // the counters
   auto us = [&] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(); };
   if (trace) fprintf(stderr, "[irdn] %zu chunks enqueued at %.1f us\n", chunks.size(), us());
   if (use_delta) {
     const int nt = copy_threads();
+    double ratio = 0.0;
     for (size_t i = 0; i < chunks.size(); ++i) {
       IRDN_CUDA(cudaEventSynchronize(ev_done[i]));
       if (trace) fprintf(stderr, "[irdn]   chunk %zu ready %.1f us", i, us());
       const int64_t off = chunk_off(chunks[i]), cnt = chunk_cnt(chunks[i]);
-      const uint8_t* src = static_cast<const uint8_t*>(ws.delta_h) + delta_off[i];
+      uint8_t* src = ws.delta_h + delta_off[i];
+      const int64_t total = *reinterpret_cast<const uint32_t*>(src), budget = delta_budget(cnt);
+      if (total > budget) {  // more changed pixels than budgeted: fetch the rest of the values
+        const int64_t vo = delta::values_offset(cnt) + budget * (int64_t)sizeof(T);
+        const size_t extra = (size_t)(total - budget) * sizeof(T);
+        IRDN_CUDA(cudaMemcpyAsync(src + vo, ws.delta_d + delta_off[i] + vo, extra, cudaMemcpyDeviceToHost,
+                                  ws.s_d2h));
+        IRDN_CUDA(cudaStreamSynchronize(ws.s_d2h));
+        d2h_bytes += extra;
+      }
+      ratio = std::max(ratio, (double)total / (double)cnt);
       if constexpr (sizeof(T) == 1)
-        d2h_bytes += irdn_delta_decode_host_u8(src, h_in + off, h_out + off, cnt, nt, 1);
+        irdn_delta_decode_host_u8(src, h_in + off, h_out + off, cnt, nt, 1);
       else
-        d2h_bytes += irdn_delta_decode_host_u16(src, h_in + off, h_out + off, cnt, nt, 1);
-      if (trace) fprintf(stderr, " decoded %.1f us (%lld px)\n", us(), (long long)cnt);
+        irdn_delta_decode_host_u16(src, h_in + off, h_out + off, cnt, nt, 1);
+      if (trace)
+        fprintf(stderr, " decoded %.1f us (%lld px, %lld changed)\n", us(), (long long)cnt, (long long)total);
     }
+    ws.delta_ratio = ratio;
   } else {
     d2h_bytes += nbytes;
   }
@@ -693,6 +711,7 @@ static int delta_encode(const T* d_in, const T* d_out, int64_t n, void* d_region
   int rc = check_device(nullptr);
   if (rc) return rc;
   const int vec = (((uintptr_t)d_in | (uintptr_t)d_out) & 15) == 0;
+  IRDN_CUDA(cudaMemsetAsync(d_region, 0, 16, static_cast<cudaStream_t>(stream)));
   delta::encode_kernel<T><<<(unsigned)delta::nblocks(n), delta::THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
       d_in, d_out, n, static_cast<uint8_t*>(d_region), vec);
   IRDN_CUDA(cudaGetLastError());

@@ -20,30 +20,33 @@ BLK = 4096
 
 
 def region_model(a: np.ndarray, o: np.ndarray) -> tuple[np.ndarray, int]:
-    """numpy restatement of the region layout (delta.cuh header); returns (region, bytes written)."""
+    """numpy restatement of the region layout (delta.cuh header), blocks in order; returns
+    (region, bytes carrying data = fixed part + total values)."""
     n = a.size
     s = a.itemsize
     nb = (n + BLK - 1) // BLK
-    cb = (nb * 4 + 15) // 16 * 16
-    moff = cb
-    voff = cb + nb * BLK // 8
-    reg = np.zeros(voff + nb * BLK * s, np.uint8)
-    counts = reg[:nb * 4].view(np.uint32)
-    written = cb
+    tb = (nb * 4 + 15) // 16 * 16
+    moff = 16 + 2 * tb
+    voff = moff + nb * BLK // 8
+    reg = np.zeros((voff + n * s + 15) // 16 * 16, np.uint8)
+    counts = reg[16:16 + nb * 4].view(np.uint32)
+    offsets = reg[16 + tb:16 + tb + nb * 4].view(np.uint32)
+    total = 0
     for b in range(nb):
         sl = slice(b * BLK, min(n, (b + 1) * BLK))
         ch = a[sl] != o[sl]
         c = int(ch.sum())
         counts[b] = c
+        offsets[b] = total
         if not c:
             continue
         bits = np.zeros(BLK, np.uint8)
         bits[: ch.size] = ch
         reg[moff + b * 512: moff + (b + 1) * 512] = np.packbits(bits, bitorder="little")
-        vals = o[sl][ch]
-        reg[voff + b * BLK * s: voff + b * BLK * s + c * s] = vals.view(np.uint8)
-        written += 512 + (c * s + 15) // 16 * 16
-    return reg, written
+        reg[voff + total * s: voff + (total + c) * s] = o[sl][ch].view(np.uint8)
+        total += c
+    reg[:4].view(np.uint32)[0] = total
+    return reg, voff + total * s
 
 
 def _case(n, dtype, frac, seed):
@@ -82,7 +85,7 @@ def test_decode_ignores_stale_masks_of_unchanged_blocks():
     o[BLK:2 * BLK] = a[BLK:2 * BLK]
     reg, _ = region_model(a, o)
     nb = 5
-    moff = (nb * 4 + 15) // 16 * 16
+    moff = 16 + 2 * ((nb * 4 + 15) // 16 * 16)
     reg[moff + 512: moff + 1024] = 0xFF  # stale mask of block 1
     out = np.empty_like(a)
     lib.irdn_delta_decode_u16(reg.ctypes.data, a.ctypes.data, out.ctypes.data, a.size, 1)
@@ -118,9 +121,10 @@ def test_encode_kernel_matches_model(dtype):
                         dreg.data_ptr(), None)
                 _native.check(rc)
                 got = dreg.cpu().numpy()
-                # compare what the device writes: counts, masks and values of changed blocks
+                # total and per-block counts are deterministic (block order of the values is not)
                 nb = (n + BLK - 1) // BLK
-                assert np.array_equal(got[:nb * 4], reg[:nb * 4])
+                assert np.array_equal(got[:4], reg[:4])
+                assert np.array_equal(got[16:16 + nb * 4], reg[16:16 + nb * 4])
                 out = np.empty_like(a)
                 dec = (lib.irdn_delta_decode_u8 if dtype == np.uint8 else lib.irdn_delta_decode_u16)(
                     got.ctypes.data, a.ctypes.data, out.ctypes.data, n, 1)
@@ -161,8 +165,16 @@ def test_run_filter_full_vs_sparse_return():
                 assert gst == wst
                 assert h2d_d == h2d_f == img.nbytes
                 assert d2h_f == img.nbytes + 16
-                changed = int((want != img).sum())
-                assert d2h_d <= img.nbytes // (8 * img.itemsize) + changed * img.itemsize + 16 * (img.size // BLK + 2) + 16 + 4 * (img.size // BLK + 4)
+                # sparse: per chunk the fixed part (~n/8 + 8 bytes per block) + a value budget; far
+                # below the full copy for FNR on these scenes
+                if method == 0:  # the value budget follows the last call's changed fraction
+                    again, _, (_, d2h_2) = _run(lib, img, cfg.k, method, passes)
+                    assert np.array_equal(again, want)
+                    changed = int((want != img).sum())
+                    nchunk_max = 16 + img.shape[0]
+                    bound = img.size // 8 + img.size // 512 + changed * 1.15 * img.itemsize + \
+                        nchunk_max * (2 * BLK * img.itemsize + 64) + 16
+                    assert d2h_2 <= bound, (name, d2h_2, bound)
                 # pageable and pinned caller buffers through the sparse return
                 import torch
 
