@@ -159,6 +159,7 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.one = 1u;
   p.debug = getenv("IRDN_DEBUG") ? atoi(getenv("IRDN_DEBUG")) : 0;
   p.full_tiles = 0;
+  p.static_rounds = 0;
   p.debug_buf = nullptr;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
@@ -242,6 +243,16 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   if (ntiles <= ctas * wk::WARPS || ntiles >= 8LL * ctas * wk::WARPS) split = 0;
   split = std::min(split, ntiles);
   p.full_tiles = (int)(ntiles - split);
+  // Static rounds: warp w takes tiles w, w + nwarps, ... without the scheduler atomic (its
+  // round trip stalls the warp before every tile's TMA issue); the rest of the pool is
+  // handed out dynamically so the tail stays balanced.
+  {
+    static const int srounds_env = getenv("IRDN_STATIC_ROUNDS") ? atoi(getenv("IRDN_STATIC_ROUNDS")) : -1;
+    const long long nwarps = ctas * wk::WARPS;
+    long long sr = srounds_env >= 0 ? srounds_env : 1;
+    p.static_rounds = (int)std::max<long long>(0, std::min<long long>(sr, ntiles / nwarps));
+    if (srounds_env < 0 && p.static_rounds == 0) p.static_rounds = 1;  // a short pool: one static round
+  }
   *taken = true;
   cudaError_t e = launch_pdl(wk::fnr_warp_kernel<T, K>, dim3((unsigned)ctas), dim3(wk::THREADS), G::SMEM, s, in_map, p);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -309,6 +320,7 @@ inline int launch_k3_th(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, 
   p.one = 1u;
   p.debug = 0;
   p.full_tiles = 0;
+  p.static_rounds = 0;
   p.debug_buf = nullptr;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;

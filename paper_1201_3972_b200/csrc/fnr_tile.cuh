@@ -85,6 +85,7 @@ struct TileParams {
   uint32_t one;         // 1, opaque to the compiler (keeps adds as IMAD on the FMA pipe)
   int32_t debug;        // experiments only: 1 = skip the median stage, 2 = skip the network
   int32_t full_tiles;   // warp kernel: tiles [0, full_tiles) are full height, the rest half-height halves
+  int32_t static_rounds;  // warp kernel: warp w takes tiles w + k * nwarps for k < static_rounds, then dynamic
   unsigned long long* debug_buf;  // experiments only (IRDN_TIMELINE builds): per-warp timeline
 };
 

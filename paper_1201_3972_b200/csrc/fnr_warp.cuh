@@ -228,8 +228,15 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
 
   // lane 0: grab a warp tile, publish it beside the stage, start its TMA load (or
   // arrive empty past the end); the mbarrier's release/acquire publishes the info.
+  const int nwarps = (int)gridDim.x * WARPS, gwarp = (int)blockIdx.x * WARPS + warp;
+  int taken = 1;  // tiles this warp has taken (the first one below)
   auto refill = [&](int stage, int pre = -1) {
-    const int t = pre >= 0 ? pre : (int)atomicAdd(p.sched, 1u);
+    int t = pre;
+    if (t < 0) {
+      t = taken < p.static_rounds ? gwarp + taken * nwarps
+                                  : (int)atomicAdd(p.sched, 1u) + p.static_rounds * nwarps;
+      ++taken;
+    }
     WTile ti;
     ti.t = t;
     if (t < ntiles) {
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
   int first = 0;
   if (lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&in_map) : "memory");
-    first = (int)atomicAdd(p.sched, 1u);
+    first = p.static_rounds > 0 ? gwarp : (int)atomicAdd(p.sched, 1u);
     if (first < ntiles) {
       const WTile f = tile_of(p, first, tiles_per_frame);
       asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(&in_map),
