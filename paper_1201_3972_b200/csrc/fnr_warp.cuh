@@ -126,17 +126,46 @@ __device__ __forceinline__ void fix_edges_warp(T* s_in, int gx_lo, int gy_lo, in
 }
 
 // Detector over the warp tile (tile::detect_strip with this box geometry).
+//
+// Per input row: the K-wide horizontal min / max of the lane's column pair (2J+1 aligned
+// words, odd offsets shifted in). Vertically, output rows are produced in pairs (j, j+1)
+// that share the K-2 input rows j+1 .. j+2r-1: one reduction over those, then one
+// 3-input op per output for the two rows each adds — (K-3)/2 + 2 ops per two rows instead
+// of K-1. Measured (tools/ab.sh): c3 (7x7) 689.7 -> 684.5 us, but c2 (5x5) 40.2 -> 40.5 us
+// and c4 (11x11) 251.2 -> 253.8 us, so by default only K = 7 pairs its rows
+// (IRDN_VPAIR=0: never, 1: every K).
+#ifndef IRDN_VPAIR
+#define IRDN_VPAIR -1
+#endif
 template <typename T, int K, bool FULL, int ROWS = WH>
 __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t pitch, int valid_rows, bool ok0,
                                        bool ok1, uint32_t (&flags)[2], uint32_t one) {
   static_assert(WH == 16 || WH == 32, "one or two 16-row flag words");
+  static_assert(ROWS % 2 == 0, "output rows are produced in pairs");
   using G = Geo<T, K>;
   constexpr int r = G::r, BOXW = G::BOXW;
   constexpr int J = (r + 1) / 2;
+  constexpr bool VPAIR = IRDN_VPAIR < 0 ? K == 7 : IRDN_VPAIR != 0;
+  constexpr int KR = VPAIR ? K + 1 : K;  // ring of per-row horizontal results
+  constexpr int CR = r + 2;                   // ring of centre words
   const uint32_t m1 = 0u - one, k65536 = one << 16, k2p31 = one << 31;
-  uint32_t rmin[K], rmax[K], rcen[r + 1];
+  uint32_t rmin[KR], rmax[KR], rcen[CR];
   flags[0] = flags[1] = 0u;
   const T* rowp = s_in + c0;
+  // flag test and signal-pixel store of output row y (window min vmn, max vmx, centre c)
+  auto emit = [&](int y, uint32_t vmn, uint32_t vmx, uint32_t c) {
+    // lane of m == 0 <=> centre is the window min or max (no borrow: vmn <= c <= vmx)
+    const uint32_t m = IRDN_DET_FMA ? vmin2(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c)) : vmin2(c - vmn, vmx - c);
+    // m <= 0x7FFF per lane, so +0x7FFF sets bit 15 iff m != 0
+    const uint32_t e = IRDN_DET_FMA ? fma_add(m, one, 0x7FFF7FFFu) : m + 0x7FFF7FFFu;
+    uint32_t sh;
+    if (IRDN_DET_FMA) asm("mul.hi.u32 %0, %1, %2;" : "=r"(sh) : "r"(flags[y >> 4]), "r"(k2p31));
+    else sh = flags[y >> 4] >> 1;
+    flags[y >> 4] = (sh & 0x7FFF7FFFu) | (~e & 0x80008000u);  // row i ends at bits i / 16 + i
+    if (FULL) tile::store_pair_g<T>(outp, c, true, true);
+    else if (y < valid_rows) tile::store_pair_g<T>(outp, c, ok0, ok1);
+    outp += pitch;
+  };
 #pragma unroll
   for (int s = 0; s < ROWS + 2 * r; ++s) {
     uint32_t wd[2 * J + 1];
@@ -148,24 +177,26 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
       ops[d + r] = (d & 1) == 0 ? wd[J + d / 2]
                    : (IRDN_DET_FMA ? shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536)
                                    : tile::prmt(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], 0x5432u));
-    rmin[s % K] = tile::reduce_min<K>(ops);
-    rmax[s % K] = tile::reduce_max<K>(ops);
-    rcen[s % (r + 1)] = wd[J];
-    if (s >= 2 * r) {
+    rmin[s % KR] = tile::reduce_min<K>(ops);
+    rmax[s % KR] = tile::reduce_max<K>(ops);
+    rcen[s % CR] = wd[J];
+    if constexpr (VPAIR) {
+      if (s >= 2 * r + 1 && ((s - 2 * r - 1) & 1) == 0) {
+        const int y = s - 2 * r - 1;  // output rows y, y + 1 = input rows y .. y + 2r + 1 (= s)
+        uint32_t am[K - 2], ax[K - 2];
+#pragma unroll
+        for (int q = 0; q < K - 2; ++q) {
+          am[q] = rmin[(y + 1 + q) % KR];
+          ax[q] = rmax[(y + 1 + q) % KR];
+        }
+        const uint32_t amn = tile::reduce_min<K - 2>(am), amx = tile::reduce_max<K - 2>(ax);
+        const uint32_t e_mn = rmin[(y + 2 * r) % KR], e_mx = rmax[(y + 2 * r) % KR];
+        emit(y, vmin3(amn, rmin[y % KR], e_mn), vmax3(amx, rmax[y % KR], e_mx), rcen[(y + r) % CR]);
+        emit(y + 1, vmin3(amn, e_mn, rmin[s % KR]), vmax3(amx, e_mx, rmax[s % KR]), rcen[(y + 1 + r) % CR]);
+      }
+    } else if (s >= 2 * r) {
       const int y = s - 2 * r;
-      const uint32_t vmn = tile::reduce_min<K>(rmin), vmx = tile::reduce_max<K>(rmax);
-      const uint32_t c = rcen[(s - r) % (r + 1)];
-      // lane of m == 0 <=> centre is the window min or max (no borrow: vmn <= c <= vmx)
-      const uint32_t m = IRDN_DET_FMA ? vmin2(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c)) : vmin2(c - vmn, vmx - c);
-      // m <= 0x7FFF per lane, so +0x7FFF sets bit 15 iff m != 0
-      const uint32_t e = IRDN_DET_FMA ? fma_add(m, one, 0x7FFF7FFFu) : m + 0x7FFF7FFFu;
-      uint32_t sh;
-      if (IRDN_DET_FMA) asm("mul.hi.u32 %0, %1, %2;" : "=r"(sh) : "r"(flags[y >> 4]), "r"(k2p31));
-      else sh = flags[y >> 4] >> 1;
-      flags[y >> 4] = (sh & 0x7FFF7FFFu) | (~e & 0x80008000u);  // row i ends at bits i / 16 + i
-      if (FULL) tile::store_pair_g<T>(outp, c, true, true);
-      else if (y < valid_rows) tile::store_pair_g<T>(outp, c, ok0, ok1);
-      outp += pitch;
+      emit(y, tile::reduce_min<KR>(rmin), tile::reduce_max<KR>(rmax), rcen[(s - r) % CR]);
     }
   }
 }

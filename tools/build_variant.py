@@ -15,6 +15,7 @@ target = os.path.join(B.REPO, "build_variants", name + ".so")
 cmd = [B.NVCC, *B.NVCC_FLAGS, *extra, "-I", os.path.join(B.REPO, "include"), "-o", target,
        *[os.path.join(B.CSRC, f) for f in B.CUDA_SOURCES]]
 res = subprocess.run(cmd, capture_output=True, text=True)
+open(target + ".log", "w").write(res.stdout + res.stderr)
 if res.returncode:
     sys.exit(res.stdout + res.stderr)
 print(target)
