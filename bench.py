@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--passes", type=int, default=1,
                     help="filter passes per step (run_filter passes; the CLI default is 2). value counts "
                          "pixel-passes per second")
+    ap.add_argument("--multipass", action="store_true",
+                    help="passes > 1 as ONE persistent multi-pass launch (irdn_set_multipass; DESIGN.md §9)")
     ap.add_argument("--path", default="filter", choices=["filter", "noise", "sqerr"],
                     help="filter (default, the BASELINE metric) or a widened row (bench_aux.py)")
     return ap.parse_args()
@@ -331,6 +333,8 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = _native.load_lib()
+    if args.multipass:
+        lib.irdn_set_multipass(1)
     steps = args.steps if args.steps is not None else default_steps(cfg)
     warmup = max(3, args.warmup)
     bpp = cfg.bytes_per_pixel
@@ -359,7 +363,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
         if passes == 1:
             rc = fn(ins[i % R].data_ptr(), outs[i % R].data_ptr(), B, H, W, W, W, cfg.k, 0,
                     counts.data_ptr(), sptr)
-        else:  # run_filter over device buffers: `passes` back-to-back PDL launches via tmp
+        else:  # run_filter over device buffers: all passes in one multi-pass launch (via tmp)
             rc = dfn(ins[i % R].data_ptr(), outs[i % R].data_ptr(), tmp.data_ptr(), B, H, W, cfg.k, 0, passes,
                      counts.data_ptr(), sptr)
         if rc != 0:
@@ -369,6 +373,12 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
         for i in range(warmup):
             launch(i)
     torch.cuda.synchronize(dev)
+    # kernel launches per step (1 for passes > 1 too: all passes run in one multi-pass launch)
+    lib.irdn_reset_launch_count()
+    with torch.cuda.stream(stream):
+        launch(0)
+    torch.cuda.synchronize(dev)
+    per_step = int(lib.irdn_launch_count())
 
     graph = None
     if not args.no_graph:
@@ -409,7 +419,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
     torch.cuda.synchronize(dev)
     sampler.stop()
     eager_launches = int(lib.irdn_launch_count())
-    gpu_launches = ((steps // R) * R + (steps % R)) * passes if graph is not None else eager_launches
+    gpu_launches = ((steps // R) * R + (steps % R)) * per_step if graph is not None else eager_launches
     elapsed_ms = ev0.elapsed_time(ev1)
     if world > 1:
         import torch.distributed as dist
@@ -542,6 +552,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
             "data": "synthetic (seeded IR scenes, DESIGN.md §5)",
             "config": {"workload": workload_desc(cfg), "frames_per_gpu": B, "height": H, "width": W,
                        "k": cfg.k, "method": "fnr", "passes": passes,
+                       **({"multipass_launch": True} if args.multipass and passes > 1 else {}),
                        "detected_per_step": det // steps,
                        "l2": f"rotating {R} distinct in/out batch buffers "
                              f"({2 * R * batch_bytes / 1e6:.0f} MB > 2x L2)" if R > 1 else

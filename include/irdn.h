@@ -168,6 +168,16 @@ IRDN_API int irdn_sq_err_sum_u16(const uint16_t* d_a, const uint16_t* d_b, int64
                                  unsigned long long* d_sum, void* stream);
 
 /*
+ * passes > 1 (irdn_run_filter_*, irdn_run_filter_device_*): 1 = all passes in ONE
+ * persistent launch of the warp kernel, a tile of pass q starting as soon as the tiles of
+ * pass q-1 under its window box have published their output (filters.py:96-100: every
+ * pass still reads the complete previous output); 0 (default) = one launch per pass,
+ * back to back with programmatic dependent launch — measured faster on B200 (DESIGN.md
+ * §9). Returns the previous setting. Process-wide; IRDN_MULTIPASS=1 sets it initially.
+ */
+IRDN_API int32_t irdn_set_multipass(int32_t on);
+
+/*
  * Result return of irdn_run_filter_*: 0 = auto (sparse for FNR on u16 frames, else full copy),
  * 1 = full device->host copy of the output, 2 = sparse. Sparse: the device sends only
  * the output pixels that differ from the input (a per-4096-pixel count, a change

@@ -49,7 +49,7 @@ EXPORTED = [
     "irdn_run_filter_device_u16", "irdn_launch_count", "irdn_reset_launch_count",
     "irdn_set_force_generic", "irdn_inject_impulse_u8", "irdn_sq_err_sum_u8", "irdn_sq_err_sum_u16",
     "irdn_set_host_return", "irdn_last_transfer", "irdn_delta_region_bytes", "irdn_delta_encode_u8",
-    "irdn_delta_encode_u16", "irdn_delta_decode_u8", "irdn_delta_decode_u16",
+    "irdn_delta_encode_u16", "irdn_delta_decode_u8", "irdn_delta_decode_u16", "irdn_set_multipass",
 ]
 
 HOST_RETURN = {"auto": 0, "full": 1, "delta": 2}
@@ -92,6 +92,8 @@ def _declare(l: ctypes.CDLL) -> None:
         f.restype = ctypes.c_int
         f.argtypes = [vp, vp, i64, vp, vp]
     u64 = ctypes.c_uint64
+    l.irdn_set_multipass.restype = i32
+    l.irdn_set_multipass.argtypes = [i32]
     l.irdn_set_host_return.restype = i32
     l.irdn_set_host_return.argtypes = [i32]
     l.irdn_last_transfer.restype = None

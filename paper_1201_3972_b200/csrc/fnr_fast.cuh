@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <vector>
 #include "fnr_common.cuh"
 #include "fnr_tile.cuh"
 #include "fnr_k3.cuh"
@@ -261,6 +262,157 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
     return 1;
   }
   return 0;
+}
+
+// Completion flags of the multi-pass kernel: one grow-only buffer per (device, stream).
+// Word 0 is the stream's launch epoch: a launch reads it after griddepcontrol.wait (the
+// previous launch on the stream has completed), tags its flags with epoch + 1 and its last
+// warp stores epoch + 1 back, so stale flags never match — also across CUDA-graph
+// replays, whose kernel parameters are frozen. Distinct streams never share a buffer.
+constexpr size_t kMpFlagsOff = 32;  // tile flags start one 128-byte line after the epoch
+inline unsigned int* mp_flags(int dev, cudaStream_t s, size_t words) {
+  struct Entry { int dev; cudaStream_t s; unsigned int* p; size_t cap; };
+  static std::mutex mu;
+  static std::vector<Entry> pool;
+  std::lock_guard<std::mutex> lock(mu);
+  Entry* e = nullptr;
+  for (Entry& x : pool)
+    if (x.dev == dev && x.s == s) e = &x;
+  if (!e) {
+    pool.push_back({dev, s, nullptr, 0});
+    e = &pool.back();
+  }
+  words += kMpFlagsOff;
+  if (e->cap < words) {
+    // a larger buffer for this stream: free the old one once the stream has drained it
+    if (e->p) {
+      cudaStreamSynchronize(s);
+      cudaFree(e->p);
+    }
+    e->p = nullptr;
+    e->cap = 0;
+    void* q = nullptr;
+    if (cudaMalloc(&q, words * sizeof(unsigned int)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    cudaMemset(q, 0, words * sizeof(unsigned int));
+    cudaDeviceSynchronize();
+    e->p = static_cast<unsigned int*>(q);
+    e->cap = words;
+  }
+  return e->p;
+}
+
+// All `passes` passes of run_filter in one persistent launch of the warp kernel
+// (fnr_warp_mp_kernel); d_tmp has the geometry of d_out.
+template <typename T, int K>
+inline int launch_warp_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, int method, int passes,
+                          unsigned long long* counts, cudaStream_t s, bool* taken) {
+  using G = wk::Geo<T, K>;
+  *taken = false;
+  CUtensorMap maps[3];
+  if (!make_map<T>(&maps[0], d_in, g.width, g.in_rows, g.batch, g.in_pitch, g.in_frame_stride, G::BOXW, G::BOXH) ||
+      !make_map<T>(&maps[1], d_tmp, g.width, g.in_rows, g.batch, g.out_pitch, g.out_frame_stride, G::BOXW,
+                   G::BOXH) ||
+      !make_map<T>(&maps[2], d_out, g.width, g.in_rows, g.batch, g.out_pitch, g.out_frame_stride, G::BOXW,
+                   G::BOXH))
+    return 0;
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    cudaFuncSetAttribute(wk::fnr_warp_mp_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wk::fnr_warp_mp_kernel<T, K>, wk::THREADS, G::SMEM) !=
+            cudaSuccess ||
+        n < 1) {
+      cudaGetLastError();
+      n = 1;
+    }
+    blocks_per_sm = n;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  unsigned int* sched = sched_slot(dev);
+  if (!sched) return 0;
+  tile::TileParams p;
+  p.out = d_out;
+  p.out_pitch = g.out_pitch;
+  p.out_frame = g.out_frame_stride;
+  p.width = g.width;
+  p.height = g.height;
+  p.in_row0 = g.in_row0;
+  p.row_begin = g.row_begin;
+  p.row_end = g.row_end;
+  p.tiles_x = (g.width + wk::WW - 1) / wk::WW;
+  p.tiles_y = (g.row_end - g.row_begin + wk::WH - 1) / wk::WH;
+  p.batch = g.batch;
+  p.method = method;
+  p.counts = counts;
+  p.sched = sched;
+  p.one = 1u;
+  p.debug = 0;
+  p.debug_buf = nullptr;
+  p.passes = passes;
+  p.tmp = d_tmp;
+  const long long npass = (long long)p.tiles_x * p.tiles_y * g.batch;
+  if ((long long)passes * npass + npass > 0x7fffffffLL) return 0;
+  p.flags = mp_flags(dev, s, (size_t)(passes - 1) * (size_t)npass);
+  if (!p.flags) return 0;
+  p.epoch = 0;  // read on the device
+  const long long ctas = std::max<long long>(1, std::min<long long>((npass + wk::WARPS - 1) / wk::WARPS,
+                                                                    (long long)sms * blocks_per_sm));
+  const long long nwarps = ctas * wk::WARPS;
+  long long split = wk::WH == 32 ? nwarps : 0;  // half-height tail: about one tile per warp
+  if ((long long)passes * npass <= nwarps || (long long)passes * npass >= 8LL * nwarps) split = 0;
+  split = std::min(split, npass);
+  p.full_tiles = (int)(npass - split);
+  // Every tile is handed out dynamically: a tile is then always owned by a running warp,
+  // and a warp only waits on tiles of the previous pass, all handed out before its own,
+  // so the launch makes progress even when another grid holds part of the GPU (a static
+  // first tile could belong to a CTA that is not resident yet).
+  p.static_rounds = 0;
+  *taken = true;
+  cudaError_t e = launch_pdl(wk::fnr_warp_mp_kernel<T, K>, dim3((unsigned)ctas), dim3(wk::THREADS), G::SMEM, s,
+                             maps[0], maps[1], maps[2], p);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_fast_err = cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
+
+// Multi-pass launch for the warp-kernel family (u16: k = 3..11; u8: k = 5..11), whole
+// frames only; false when the layout or k does not qualify (the caller then runs the
+// passes as separate launches). Opt-in (irdn_set_multipass / IRDN_MULTIPASS=1): measured
+// slower than back-to-back single-pass launches on B200.
+inline int kernel_family();
+template <typename T>
+inline bool try_launch_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, int k, int method, int passes,
+                          unsigned long long* counts, cudaStream_t s, int* rc) {
+  if (passes < 2 || kernel_family() != 1) return false;
+  const size_t bpp = sizeof(T);
+  if (((uintptr_t)d_in & 15) || ((uintptr_t)d_out & 15) || ((uintptr_t)d_tmp & 15)) return false;
+  if ((g.in_pitch * bpp) % 16 || (g.out_pitch * bpp) % 16) return false;
+  if ((g.in_frame_stride * bpp) % 16 || (g.out_frame_stride * bpp) % 16) return false;
+  if (g.width < 16 || g.height < 1 || g.row_begin != 0 || g.row_end != g.height || g.in_rows != g.height) return false;
+  bool taken = false;
+  int e = 0;
+  switch (k) {
+    case 3:
+      if constexpr (sizeof(T) == 2) e = launch_warp_mp<T, 3>(d_in, d_out, d_tmp, g, method, passes, counts, s, &taken);
+      else return false;
+      break;
+    case 5: e = launch_warp_mp<T, 5>(d_in, d_out, d_tmp, g, method, passes, counts, s, &taken); break;
+    case 7: e = launch_warp_mp<T, 7>(d_in, d_out, d_tmp, g, method, passes, counts, s, &taken); break;
+    case 9: e = launch_warp_mp<T, 9>(d_in, d_out, d_tmp, g, method, passes, counts, s, &taken); break;
+    case 11: e = launch_warp_mp<T, 11>(d_in, d_out, d_tmp, g, method, passes, counts, s, &taken); break;
+    default: return false;
+  }
+  if (!taken) return false;
+  *rc = e ? 2 : 0;
+  return true;
 }
 
 // Kernel family for k = 5..11 (and k = 3 on u16): the warp-autonomous kernel; the

@@ -86,6 +86,11 @@ struct TileParams {
   int32_t debug;        // experiments only: 1 = skip the median stage, 2 = skip the network
   int32_t full_tiles;   // warp kernel: tiles [0, full_tiles) are full height, the rest half-height halves
   int32_t static_rounds;  // warp kernel: warp w takes tiles w + k * nwarps for k < static_rounds, then dynamic
+  // multi-pass warp kernel (fnr_warp_mp_kernel): `passes` passes in one launch
+  int32_t passes;
+  void* tmp;              // ping-pong buffer (same geometry as out)
+  unsigned int* flags;    // [0] launch epoch of the stream; from [32]: (passes - 1) x tiles-per-pass flags
+  uint32_t epoch;         // unused on the host (the kernel derives the epoch from flags[0])
   unsigned long long* debug_buf;  // experiments only (IRDN_TIMELINE builds): per-warp timeline
 };
 

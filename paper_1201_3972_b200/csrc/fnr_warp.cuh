@@ -59,7 +59,7 @@ struct Geo {
 };
 
 struct WTile {
-  int t, b, x0, y0, rows;
+  int t, b, x0, y0, rows, pass;
 };
 
 // Tile t of the pass. The pool ends in half-height tiles (the halves of the last
@@ -82,6 +82,30 @@ __device__ __forceinline__ WTile tile_of(const tile::TileParams& p, int t, int t
   ti.x0 = (tt - ty * p.tiles_x) * WW;
   ti.y0 = p.row_begin + ty * WH + dy;
   ti.rows = rows;
+  return ti;
+}
+
+// Multi-pass launch: tiles [0, (P-1) N) are the full tiles of passes 0 .. P-2 in order
+// (N tiles per pass), the rest is the last pass with its half-height tail (tile_of).
+__device__ __forceinline__ WTile tile_of_mp(const tile::TileParams& p, int t, int tiles_per_frame) {
+  const int N = tiles_per_frame * p.batch;
+  const int early = (p.passes - 1) * N;
+  if (t >= early) {
+    WTile ti = tile_of(p, t - early, tiles_per_frame);
+    ti.t = t;
+    ti.pass = p.passes - 1;
+    return ti;
+  }
+  WTile ti;
+  ti.t = t;
+  ti.pass = t / N;
+  const int u = t - ti.pass * N;
+  ti.b = u / tiles_per_frame;
+  const int tt = u - ti.b * tiles_per_frame;
+  const int ty = tt / p.tiles_x;
+  ti.x0 = (tt - ty * p.tiles_x) * WW;
+  ti.y0 = p.row_begin + ty * WH;
+  ti.rows = WH;
   return ti;
 }
 
@@ -239,9 +263,15 @@ __device__ __forceinline__ uint32_t medians(const T* s_in, const uint16_t* q, in
   return replaced;
 }
 
-template <typename T, int K>
-__global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant__ CUtensorMap in_map,
-                                                           const tile::TileParams p) {
+// MP = false: one pass from map0 into p.out. MP = true: p.passes passes in one persistent
+// launch (pass 0 reads map0 = input; pass q > 0 reads the output of pass q-1 through map1
+// (= p.tmp) or map2 (= p.out); the last pass writes p.out). A tile of pass q > 0 starts
+// once the (up to) 3 x 3 tiles of pass q-1 under its box have published their flags, so
+// the passes overlap tile by tile instead of meeting at a kernel boundary.
+template <typename T, int K, bool MP>
+__device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtensorMap* map1, const CUtensorMap* map2,
+                                          const tile::TileParams& p) {
+  static_assert(!MP || NSTAGE == 1, "a warp waiting on pass dependencies must hold no other tile");
   using G = Geo<T, K>;
   constexpr int r = G::r, R = G::R, BOXW = G::BOXW;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -253,12 +283,17 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
   WTile* s_info = reinterpret_cast<WTile*>(wsm + G::INFO_OFF);
 
   const int tiles_per_frame = p.tiles_x * p.tiles_y;
-  const int ntiles = p.full_tiles + 2 * (tiles_per_frame * p.batch - p.full_tiles);
+  const int npass = tiles_per_frame * p.batch;  // full tiles per pass
+  const int ntiles = (MP ? (p.passes - 1) * npass : 0) + p.full_tiles + 2 * (npass - p.full_tiles);
   const bool fnr = p.method == 0;
+  // pass q writes out when (P-1-q) is even, else tmp (the last pass lands in out)
+  auto dst_is_out = [&](int q) { return !MP || ((p.passes - 1 - q) & 1) == 0; };
+  auto tile_at = [&](int t) { return MP ? tile_of_mp(p, t, tiles_per_frame) : tile_of(p, t, tiles_per_frame); };
   uint32_t replaced = 0, detected = 0;
 
   // lane 0: grab a warp tile, publish it beside the stage, start its TMA load (or
   // arrive empty past the end); the mbarrier's release/acquire publishes the info.
+  uint32_t epoch = 0;  // MP: this launch's flag value (lane 0; read after griddepcontrol.wait)
   const int nwarps = (int)gridDim.x * WARPS, gwarp = (int)blockIdx.x * WARPS + warp;
   int taken = 1;  // tiles this warp has taken (the first one below)
   auto refill = [&](int stage, int pre = -1) {
@@ -271,10 +306,37 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
     WTile ti;
     ti.t = t;
     if (t < ntiles) {
-      ti = tile_of(p, t, tiles_per_frame);
+      ti = tile_at(t);
+      const CUtensorMap* src = map0;
+      if (MP && ti.pass > 0) {
+        // wait for the pass-(q-1) tiles under this tile's box, then read their output
+        const int tx = ti.x0 / WW, ty = (ti.y0 - p.row_begin) / WH;
+        const unsigned int* fl = p.flags + 32 + (size_t)(ti.pass - 1) * npass + (size_t)ti.b * tiles_per_frame;
+        // the (up to) 9 flags with independent relaxed loads, one fence once all match
+        // (chained acquire loads would serialise nine L2 round trips per tile)
+        const int y_lo = max(ty - 1, 0), y_hi = min(ty + 1, p.tiles_y - 1);
+        const int x_lo = max(tx - 1, 0), x_hi = min(tx + 1, p.tiles_x - 1);
+        for (;;) {
+          bool ready = true;
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+              const int y = min(y_lo + dy, y_hi), x = min(x_lo + dx, x_hi);
+              uint32_t v;
+              asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl + y * p.tiles_x + x) : "memory");
+              ready &= v == epoch;
+            }
+          if (ready) break;
+          __nanosleep(64);
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire: the flags' release stores
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy writes -> TMA reads
+        src = dst_is_out(ti.pass - 1) ? map2 : map1;
+      }
       s_info[stage] = ti;
       tile::mbar_expect_tx(&s_bar[stage], G::IN_BYTES);
-      tile::tma_load_3d(wsm + stage * G::STAGE, &in_map, &s_bar[stage], ti.x0 - R, ti.y0 - r - p.in_row0, ti.b);
+      tile::tma_load_3d(wsm + stage * G::STAGE, src, &s_bar[stage], ti.x0 - R, ti.y0 - r - p.in_row0, ti.b);
     } else {
       s_info[stage] = ti;
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tile::smem_u32(&s_bar[stage])) : "memory");
@@ -286,17 +348,21 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
   // issued after griddepcontrol.wait.
   int first = 0;
   if (lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&in_map) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map0) : "memory");
     first = p.static_rounds > 0 ? gwarp : (int)atomicAdd(p.sched, 1u);
     if (first < ntiles) {
-      const WTile f = tile_of(p, first, tiles_per_frame);
-      asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(&in_map),
+      const WTile f = tile_at(first);
+      asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(map0),
                    "r"(f.x0 - R), "r"(f.y0 - r - p.in_row0), "r"(f.b)
                    : "memory");
     }
   }
   pdl_wait_and_trigger();
   if (lane == 0) {
+    if (MP) {
+      epoch = *reinterpret_cast<volatile unsigned int*>(p.flags) + 1u;
+      if (epoch == 0u) epoch = 1u;
+    }
 #pragma unroll
     for (int s = 0; s < NSTAGE; ++s) tile::mbar_init(&s_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -306,7 +372,6 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
   __syncwarp();
 
   const int c0 = 2 * lane + R;  // smem column of this lane's first pixel
-  T* const out_base = reinterpret_cast<T*>(p.out);
 
 #ifdef IRDN_TIMELINE
   uint64_t t_wait, t_ready, t_det = 0, t_done;
@@ -334,6 +399,7 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
     const int gx_lo = ti.x0 - R, gy_lo = ti.y0 - r;
     if (gx_lo < 0 || gy_lo < 0 || gx_lo + BOXW > p.width || gy_lo + G::BOXH > p.height)
       fix_edges_warp<T, K>(s_in, gx_lo, gy_lo, p.width, p.height, lane);
+    T* const out_base = reinterpret_cast<T*>(dst_is_out(MP ? ti.pass : 0) ? p.out : p.tmp);
     T* const out_tile = out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.y0 - p.row_begin) * p.out_pitch + ti.x0;
     const bool ok0 = 2 * lane < valid_w, ok1 = 2 * lane + 1 < valid_w;
     int n;
@@ -416,6 +482,17 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
       d[5] = ((unsigned long long)(blockIdx.x * WARPS + warp) << 16) | smid;
     }
 #endif
+    if (MP && ti.pass < p.passes - 1) {
+      // publish this tile's output to the next pass: every lane's stores, then the flag
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        const int tx = ti.x0 / WW, ty = (ti.y0 - p.row_begin) / WH;
+        unsigned int* f =
+            p.flags + 32 + (size_t)ti.pass * npass + (size_t)ti.b * tiles_per_frame + ty * p.tiles_x + tx;
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+      }
+    }
     // this stage is free: load the warp's next tile into it
     tile::fence_proxy_async();
     __syncwarp();
@@ -424,8 +501,24 @@ __global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant
   if (lane == 0 && atomicAdd(p.sched + 1, 1u) == gridDim.x * WARPS - 1) {
     p.sched[0] = 0u;
     p.sched[1] = 0u;
+    if (MP) *reinterpret_cast<volatile unsigned int*>(p.flags) = epoch;  // every warp has read the old one
   }
   if (fnr) block_add_counts<THREADS>(detected, replaced, p.counts);
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(THREADS) fnr_warp_kernel(const __grid_constant__ CUtensorMap in_map,
+                                                           const tile::TileParams p) {
+  warp_body<T, K, false>(&in_map, &in_map, &in_map, p);
+}
+
+// `p.passes` passes in one launch: in_map = input, tmp_map = p.tmp, out_map = p.out.
+template <typename T, int K>
+__global__ void __launch_bounds__(THREADS) fnr_warp_mp_kernel(const __grid_constant__ CUtensorMap in_map,
+                                                              const __grid_constant__ CUtensorMap tmp_map,
+                                                              const __grid_constant__ CUtensorMap out_map,
+                                                              const tile::TileParams p) {
+  warp_body<T, K, true>(&in_map, &tmp_map, &out_map, p);
 }
 
 }  // namespace wk

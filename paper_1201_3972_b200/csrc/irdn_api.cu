@@ -39,6 +39,8 @@ static thread_local std::string g_err;
 static thread_local uint64_t g_launches = 0;
 static thread_local uint64_t g_xfer_h2d = 0, g_xfer_d2h = 0;  // bytes moved by the last irdn_run_filter_* call
 static int32_t g_force_generic = 0;
+// passes > 1 in one multi-pass launch (fnr_warp_mp_kernel); off by default
+static int32_t g_multipass = getenv("IRDN_MULTIPASS") ? (atoi(getenv("IRDN_MULTIPASS")) != 0) : 0;
 // Host-buffer result return: 0 = auto (sparse for FNR on u16, else the full copy), 1 = full copy,
 // 2 = sparse (delta.cuh). IRDN_HOST_RETURN=full|delta|auto sets the initial value.
 static int32_t g_host_return = [] {
@@ -200,6 +202,36 @@ static int run_device(const T* d_in, T* d_out, T* d_tmp, int64_t batch, int64_t 
                       unsigned long long* d_counts, void* stream) {
   if (passes < 1) return fail(IRDN_EINVAL, "passes must be >= 1, got %d", passes);  // filters.py:92-93
   if (passes > 1 && !d_tmp) return fail(IRDN_EINVAL, "passes > 1 needs a d_tmp buffer");
+  if (passes > 1 && !g_force_generic && g_multipass) {
+    // all passes in one persistent launch of the warp kernel (tile-level pass dependencies)
+    int rc = validate(batch, height, width, k, method);
+    if (rc) return rc;
+    if (!d_in || !d_out) return fail(IRDN_EINVAL, "null buffer");
+    if (method == IRDN_METHOD_FNR && !d_counts) return fail(IRDN_EINVAL, "FNR needs d_counts[2]");
+    const size_t bytes = (size_t)(batch * height * width) * sizeof(T);
+    if (overlaps(d_in, bytes, d_out, bytes) || overlaps(d_in, bytes, d_tmp, bytes) ||
+        overlaps(d_out, bytes, d_tmp, bytes))
+      return fail(IRDN_EINVAL, "input, output and scratch buffers overlap");
+    if ((rc = check_device(nullptr))) return rc;
+    PassGeom g;
+    g.in_frame_stride = height * width;
+    g.out_frame_stride = height * width;
+    g.in_pitch = width;
+    g.out_pitch = width;
+    g.height = (int32_t)height;
+    g.width = (int32_t)width;
+    g.in_row0 = 0;
+    g.in_rows = (int32_t)height;
+    g.row_begin = 0;
+    g.row_end = (int32_t)height;
+    g.batch = (int32_t)batch;
+    int lrc = 0;
+    if (fast::try_launch_mp<T>(d_in, d_out, d_tmp, g, k, method, passes, d_counts, (cudaStream_t)stream, &lrc)) {
+      if (lrc != IRDN_OK) return fail(IRDN_ECUDA, "multi-pass kernel launch failed: %s", fast::last_error());
+      note_launch();
+      return IRDN_OK;
+    }
+  }
   const T* src = d_in;
   for (int p = 0; p < passes; ++p) {
     T* dst = ((passes - 1 - p) % 2 == 0) ? d_out : d_tmp;
@@ -806,6 +838,11 @@ int irdn_sq_err_sum_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t n, unsign
 int irdn_sq_err_sum_u16(const uint16_t* d_a, const uint16_t* d_b, int64_t n, unsigned long long* d_sum,
                         void* stream) {
   return sq_err_sum<uint16_t>(d_a, d_b, n, d_sum, stream);
+}
+int32_t irdn_set_multipass(int32_t on) {
+  int32_t prev = g_multipass;
+  g_multipass = on ? 1 : 0;
+  return prev;
 }
 int32_t irdn_set_host_return(int32_t mode) {
   int32_t prev = g_host_return;
