@@ -26,6 +26,7 @@
 #include "metrics.cuh"
 #include "noise.cuh"
 #include "delta.cuh"
+#include "fnr_large.cuh"
 
 // delta_host.cpp (host decode of the sparse result return, compiled by the host compiler)
 uint64_t irdn_delta_decode_host_u8(const uint8_t* src, const uint8_t* in, uint8_t* out, int64_t n, int threads,
@@ -121,6 +122,24 @@ static int launch_pass(const T* d_in, T* d_out, const PassGeom& g, int k, int me
     }
   }
   const int rows = g.row_end - g.row_begin;
+  if (!g_force_generic && k / 2 <= large::LMAX_R) {
+    // shared-memory tiled kernel: k >= 13, or layouts the TMA kernels cannot take
+    const long long tiles = (long long)((g.width + large::TW - 1) / large::TW) * ((rows + large::TH - 1) / large::TH);
+    if (tiles <= 0x7fffffffLL) {
+      // median search with the window in registers: up to V elements per lane (k^2 <= 32 V)
+      const int kk = k * k;
+      auto kern = kk <= 32 * 8 ? large::fnr_large_kernel<T, 8>
+                  : kk <= 32 * 16 ? large::fnr_large_kernel<T, 16>
+                  : kk <= 32 * 32 ? large::fnr_large_kernel<T, 32> : large::fnr_large_kernel<T, 0>;
+      const size_t smem = sizeof(large::Smem<T>);
+      IRDN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<dim3((unsigned)tiles, (unsigned)std::min<int>(g.batch, 65535)), large::THREADS, smem, s>>>(
+          d_in, d_out, g, k, method, d_counts);
+      IRDN_CUDA(cudaGetLastError());
+      note_launch();
+      return IRDN_OK;
+    }
+  }
   dim3 grid((g.width + 31) / 32, (rows + 7) / 8, std::min<int>(g.batch, 65535));
   if (grid.y > 65535u) return fail(IRDN_EINVAL, "frame too tall for the generic kernel");
   fnr_generic_kernel<T><<<grid, 256, 0, s>>>(d_in, d_out, g, k, method, d_counts);

@@ -411,3 +411,41 @@ def test_fnr_pass_mf_pass_accumulate_like_the_reference(cuda_ok):
             cur = step(cur, P.WindowSpec(meta["k"]), st)
         assert bytes(cur.pixels) == out.tobytes(), meta
         assert counters(st) == meta["stats"] and st.elapsed_ms == 12.5, (meta, st)
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_large_windows_and_unaligned_layouts(cuda_ok, dtype):
+    """k >= 13 and layouts the TMA kernels cannot take (pitch not a multiple of 16 bytes)
+    run the shared-memory tiled kernel (csrc/fnr_large.cuh); bit-exact vs the oracle, also
+    against the generic kernel."""
+    rng = np.random.default_rng(1313 + np.dtype(dtype).itemsize)
+    hi = 256 if dtype == np.uint8 else 16384
+    cases = [(13, 2, 70, 100), (15, 1, 40, 200), (21, 1, 64, 64), (31, 2, 33, 47), (63, 1, 90, 130),
+             (3, 2, 244, 364), (5, 1, 51, 77), (11, 1, 37, 131), (13, 1, 5, 3), (17, 1, 1, 1)]
+    for k, b, h, w in cases:
+        yy, xx = np.mgrid[0:h, 0:w]
+        img = np.broadcast_to((yy * 5 + xx * 3) % hi, (b, h, w)).astype(dtype).copy()
+        m = rng.random(img.shape) < 0.25
+        img[m] = rng.integers(0, hi, int(m.sum())).astype(dtype)
+        for method in ("fnr", "mf"):
+            want, wst = _oracle(img, k, method, 1)
+            got, gst = gpu_filter(img, k, method, 1)
+            assert np.array_equal(got, want), (k, img.shape, method)
+            assert gst == wst
+            with force_generic():
+                got2, gst2 = gpu_filter(img, k, method, 1)
+            assert np.array_equal(got2, want) and gst2 == wst
+
+
+def test_large_window_row_strips(cuda_ok):
+    import torch
+
+    img = generate(CONFIGS["c4"].with_shape(height=300, width=200), nframes=1)[0]
+    t = torch.from_numpy(img.view(np.int16)).cuda()
+    for k in (13, 21):
+        want, _ = _oracle(img, k, "fnr", 1)
+        parts = []
+        for a, b in ((0, 97), (97, 98), (98, 300)):
+            parts.append(_strip_call(t, k, a, b)[0])
+        got = torch.cat(parts, 0).cpu().numpy().view(np.uint16)
+        assert np.array_equal(got, want), k
