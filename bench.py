@@ -528,7 +528,8 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
            "api": f"irdn_run_filter_{cfg.dtype} (C ABI, include/irdn.h) on pinned host buffers; "
                   "host wall clock, call is synchronous",
            "result_return": "sparse (changed pixels only, rebuilt on the host from its input; DESIGN.md §7.1)"
-                            if bpp == 2 else "full D2H copy (auto mode for 8-bit frames, DESIGN.md §7.1)",
+                            if d2h < batch_bytes else "full D2H copy (auto mode: 8-bit frames, or < 6 host "
+                                                      "threads per GPU process; DESIGN.md §7.1)",
            "full_copy": {"value": round(full_v, 3), "d2h_bytes_per_step": full_d2h}}
     if st.detected * steps != det:
         raise AssertionError(f"counter mismatch: {st.detected}*{steps} != {det}")

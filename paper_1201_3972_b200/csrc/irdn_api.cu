@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <omp.h>
+#include <sched.h>
 #include <string>
 #include <vector>
 
@@ -303,19 +304,28 @@ static int ensure_staging(DeviceWorkspace& ws, size_t slot_bytes) {
   return IRDN_OK;
 }
 
-// Host threads for copies and the sparse-return decode: the host's threads shared out
-// between the GPUs one process each may drive (16 threads: 113 GB/s memcpy on the
-// 16-core B200 box vs 90 GB/s with 8, tools/microbench/host_probe.cu), capped at 16.
+// Host threads for copies and the sparse-return decode: the host's cores shared out between
+// the processes on this node (LOCAL_WORLD_SIZE under torchrun, else one per visible GPU),
+// capped at 16 (16 threads: 113 GB/s memcpy on the 16-core B200 box vs 90 GB/s with 8,
+// tools/microbench/host_probe.cu). Counted from the CPU affinity mask, not from
+// OMP_NUM_THREADS (torchrun sets that to 1 per rank); IRDN_COPY_THREADS overrides.
 static int copy_threads() {
   static const int nt = [] {
     const char* e = getenv("IRDN_COPY_THREADS");
     if (e) return std::max(1, atoi(e));
-    int ndev = 1;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
-      cudaGetLastError();
-      ndev = 1;
+    int hw = 0;
+    cpu_set_t cs;
+    if (sched_getaffinity(0, sizeof(cs), &cs) == 0) hw = CPU_COUNT(&cs);
+    if (hw <= 0) hw = std::max(1, omp_get_num_procs());
+    int ranks = 0;
+    if (const char* l = getenv("LOCAL_WORLD_SIZE")) ranks = atoi(l);
+    if (ranks <= 0) {
+      if (cudaGetDeviceCount(&ranks) != cudaSuccess || ranks < 1) {
+        cudaGetLastError();
+        ranks = 1;
+      }
     }
-    return std::max(1, std::min(16, omp_get_max_threads() / ndev));
+    return std::max(1, std::min(16, hw / ranks));
   }();
   return nt;
 }
@@ -466,8 +476,10 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   // auto: sparse for FNR on 16-bit frames (c2 1.23-1.27 -> 1.01 ms, c4 4.6 -> 3.3 ms per call,
   // tools/e2e_probe.py); 8-bit frames keep the full copy: rebuilding 1 B/px on the host costs
   // about what the D2H saves (c3 2.06 -> 1.98 ms, but c5 31.8 -> 37.4 ms, c1 0.050 -> 0.067 ms)
-  const bool use_delta =
-      g_host_return == 2 || (g_host_return == 0 && method == IRDN_METHOD_FNR && sizeof(T) == 2);
+  // (and only with >= 6 host threads for the rebuild: ~13 GB/s per thread, the full copy's
+  // extra cost over the H2D is ~0.2-0.4 ms per 42 MB)
+  const bool use_delta = g_host_return == 2 || (g_host_return == 0 && method == IRDN_METHOD_FNR &&
+                                                 sizeof(T) == 2 && copy_threads() >= 6);
   std::vector<int64_t> delta_off(chunks.size() + 1, 0);
   if (use_delta) {
     for (size_t i = 0; i < chunks.size(); ++i)
