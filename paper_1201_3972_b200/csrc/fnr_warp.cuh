@@ -158,6 +158,9 @@ __device__ __forceinline__ void fix_edges_warp(T* s_in, int gx_lo, int gy_lo, in
 // of K-1. Measured (tools/ab.sh): c3 (7x7) 689.7 -> 684.5 us, but c2 (5x5) 40.2 -> 40.5 us
 // and c4 (11x11) 251.2 -> 253.8 us, so by default only K = 7 pairs its rows
 // (IRDN_VPAIR=0: never, 1: every K).
+#ifndef IRDN_ROWADDR
+#define IRDN_ROWADDR -1  // -1: k <= 5 only (c2 39.93 -> 39.61 us; c3 / c4 0.0 / +0.35 %), 0 never, 1 always
+#endif
 #ifndef IRDN_VPAIR
 #define IRDN_VPAIR -1
 #endif
@@ -176,6 +179,8 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
   uint32_t rmin[KR], rmax[KR], rcen[CR];
   flags[0] = flags[1] = 0u;
   const T* rowp = s_in + c0;
+  constexpr bool ROWADDR = IRDN_ROWADDR < 0 ? K <= 5 : IRDN_ROWADDR != 0;
+  const uint32_t pitch_b = (uint32_t)(pitch * (int64_t)sizeof(T));  // < 2^32: rows of at most 2^31 pixels
   // flag test and signal-pixel store of output row y (window min vmn, max vmx, centre c)
   auto emit = [&](int y, uint32_t vmn, uint32_t vmx, uint32_t c) {
     // lane of m == 0 <=> centre is the window min or max (no borrow: vmn <= c <= vmx)
@@ -186,9 +191,16 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
     if (IRDN_DET_FMA) asm("mul.hi.u32 %0, %1, %2;" : "=r"(sh) : "r"(flags[y >> 4]), "r"(k2p31));
     else sh = flags[y >> 4] >> 1;
     flags[y >> 4] = (sh & 0x7FFF7FFFu) | (~e & 0x80008000u);  // row i ends at bits i / 16 + i
-    if (FULL) tile::store_pair_g<T>(outp, c, true, true);
-    else if (y < valid_rows) tile::store_pair_g<T>(outp, c, ok0, ok1);
-    outp += pitch;
+    if constexpr (ROWADDR) {
+      // row address = base + y * pitch (one wide multiply-add per row, y is a constant)
+      T* const rp = reinterpret_cast<T*>(reinterpret_cast<char*>(outp) + (uint64_t)(uint32_t)y * pitch_b);
+      if (FULL) tile::store_pair_g<T>(rp, c, true, true);
+      else if (y < valid_rows) tile::store_pair_g<T>(rp, c, ok0, ok1);
+    } else {
+      if (FULL) tile::store_pair_g<T>(outp, c, true, true);
+      else if (y < valid_rows) tile::store_pair_g<T>(outp, c, ok0, ok1);
+      outp += pitch;
+    }
   };
 #pragma unroll
   for (int s = 0; s < ROWS + 2 * r; ++s) {
