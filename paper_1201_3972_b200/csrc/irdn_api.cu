@@ -398,7 +398,10 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   if (overlaps(h_in, nbytes, h_out, nbytes)) return fail(IRDN_EINVAL, "input and output buffers overlap");
   if (device < 0 || device >= 64) return fail(IRDN_EINVAL, "bad device %d", device);
   int prev = 0;
-  IRDN_CUDA(cudaGetDevice(&prev));
+  {
+    const cudaError_t e = cudaGetDevice(&prev);
+    if (e != cudaSuccess) return fail(IRDN_ENODEV, "no CUDA device: %s", cudaGetErrorString(e));
+  }
   if (prev != device) IRDN_CUDA(cudaSetDevice(device));
   struct Restore {
     int d, p;

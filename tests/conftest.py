@@ -48,3 +48,9 @@ def cuda_ok():
     if not gpu_available():
         pytest.skip("needs a B200 GPU")
     return True
+
+
+@pytest.fixture
+def cuda_ok_or_none():
+    """True when a B200 is visible, False otherwise (never skips)."""
+    return bool(gpu_available())
