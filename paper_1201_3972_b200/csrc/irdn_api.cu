@@ -483,11 +483,40 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   // extra cost over the H2D is ~0.2-0.4 ms per 42 MB)
   const bool use_delta = g_host_return == 2 || (g_host_return == 0 && method == IRDN_METHOD_FNR &&
                                                  sizeof(T) == 2 && copy_threads() >= 6);
+  // Sparse return: the last chunk is rebuilt on the host after everything else has landed,
+  // so its second half comes back by a plain D2H copy into the (pinned) caller buffer
+  // instead, while the host rebuilds the first half (IRDN_SPLIT_LAST=0 disables).
+  size_t full_chunk = chunks.size();  // index of the chunk returned by a full copy (none)
+  {
+    static const int split_last = getenv("IRDN_SPLIT_LAST") ? atoi(getenv("IRDN_SPLIT_LAST")) : 1;
+    if (use_delta && split_last && chunks.size() >= 2 && is_pinned(h_out)) {
+      const Chunk c = chunks.back();
+      if (row_mode && c.y1 - c.y0 >= 2) {
+        const int64_t m = c.y0 + (c.y1 - c.y0) / 2;
+        chunks.back().y1 = m;
+        chunks.push_back({0, 1, m, c.y1});
+        full_chunk = chunks.size() - 1;
+      } else if (!row_mode && c.nf >= 2) {
+        const int64_t a = c.nf / 2;
+        chunks.back().nf = a;
+        chunks.push_back({c.f0 + a, c.nf - a, 0, height});
+        full_chunk = chunks.size() - 1;
+      }
+    }
+    while (ws.ev_in.size() < chunks.size()) {
+      cudaEvent_t a, b;
+      IRDN_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      IRDN_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      ws.ev_in.push_back(a);
+      ws.ev_done.push_back(b);
+    }
+  }
   std::vector<int64_t> delta_off(chunks.size() + 1, 0);
   if (use_delta) {
     for (size_t i = 0; i < chunks.size(); ++i)
-      delta_off[i + 1] = delta_off[i] + (row_mode ? delta::region_bytes<T>((chunks[i].y1 - chunks[i].y0) * width)
-                                                  : delta::region_bytes<T>(chunks[i].nf * frame));
+      delta_off[i + 1] = delta_off[i] + (i == full_chunk ? 0
+                                         : row_mode ? delta::region_bytes<T>((chunks[i].y1 - chunks[i].y0) * width)
+                                                    : delta::region_bytes<T>(chunks[i].nf * frame));
     if ((size_t)delta_off.back() > ws.delta_cap) {
       if (ws.delta_h) IRDN_CUDA(cudaFreeHost(ws.delta_h));
       if (ws.delta_d) IRDN_CUDA(cudaFree(ws.delta_d));
@@ -577,7 +606,7 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
       if (rc) return rc;
     }
     const int64_t off = chunk_off(c), cnt = chunk_cnt(c);
-    if (use_delta) {  // encode out vs in into the device region, DMA its fixed part + a value budget
+    if (use_delta && i != full_chunk) {  // encode out vs in into the device region, DMA its fixed part + budget
       const T* a = d_in + off;
       const T* o = d_out + off;
       const int vec = (((uintptr_t)a | (uintptr_t)o) & 15) == 0;
@@ -615,6 +644,10 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
     const int nt = copy_threads();
     double ratio = 0.0;
     for (size_t i = 0; i < chunks.size(); ++i) {
+      if (i == full_chunk) {  // came back by a full copy (synchronised with s_d2h below)
+        d2h_bytes += (uint64_t)chunk_cnt(chunks[i]) * sizeof(T);
+        continue;
+      }
       IRDN_CUDA(cudaEventSynchronize(ev_done[i]));
       if (trace) fprintf(stderr, "[irdn]   chunk %zu ready %.1f us", i, us());
       const int64_t off = chunk_off(chunks[i]), cnt = chunk_cnt(chunks[i]);
