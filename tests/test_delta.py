@@ -189,3 +189,24 @@ def test_run_filter_full_vs_sparse_return():
                 assert np.array_equal(po, want)
     finally:
         _native.set_host_return(prev)
+
+
+@pytest.mark.gpu
+def test_sparse_return_budget_overflow():
+    """The value budget follows the previous call's changed fraction: after a call that
+    changed nothing, a call that changes many pixels overflows it and fetches the rest."""
+    lib = _native.load_lib()
+    prev = _native.set_host_return("delta")
+    try:
+        flat = np.full((8, 256, 320), 1234, np.uint16)
+        out, st, _ = _run(lib, flat, 5, 0, 1)
+        assert np.array_equal(out, flat) and st[2] == 0
+        rng = np.random.default_rng(5)
+        noisy = rng.integers(0, 16384, size=(8, 256, 320)).astype(np.uint16)
+        got, gst, (_, d2h) = _run(lib, noisy, 5, 0, 1)
+        _native.set_host_return("full")
+        want, wst, _ = _run(lib, noisy, 5, 0, 1)
+        assert np.array_equal(got, want) and gst == wst
+        assert wst[2] > 8 * 4096  # far more changed pixels than the flat call's budget
+    finally:
+        _native.set_host_return(prev)
