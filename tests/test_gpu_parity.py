@@ -421,7 +421,8 @@ def test_large_windows_and_unaligned_layouts(cuda_ok, dtype):
     rng = np.random.default_rng(1313 + np.dtype(dtype).itemsize)
     hi = 256 if dtype == np.uint8 else 16384
     cases = [(13, 2, 70, 100), (15, 1, 40, 200), (21, 1, 64, 64), (31, 2, 33, 47), (63, 1, 90, 130),
-             (3, 2, 244, 364), (5, 1, 51, 77), (11, 1, 37, 131), (13, 1, 5, 3), (17, 1, 1, 1)]
+             (3, 2, 244, 364), (5, 1, 51, 77), (11, 1, 37, 131), (13, 1, 5, 3), (17, 1, 1, 1),
+             (65, 1, 70, 90), (101, 1, 20, 150)]  # k > 63: the generic kernel
     for k, b, h, w in cases:
         yy, xx = np.mgrid[0:h, 0:w]
         img = np.broadcast_to((yy * 5 + xx * 3) % hi, (b, h, w)).astype(dtype).copy()
