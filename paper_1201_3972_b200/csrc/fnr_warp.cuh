@@ -20,7 +20,10 @@
 namespace irdn {
 namespace wk {
 
-constexpr int WARPS = 2;               // warps per CTA (packaging only: no CTA barriers)
+#ifndef IRDN_WARPS
+#define IRDN_WARPS 2
+#endif
+constexpr int WARPS = IRDN_WARPS;      // warps per CTA (packaging only: no CTA barriers)
 constexpr int THREADS = 32 * WARPS;
 constexpr int WW = 64;                 // warp tile width: 32 lanes x 2 pixels
 #ifndef IRDN_WH
