@@ -24,24 +24,29 @@ sys.path.insert(0, REPO)
 from oracle import oracle  # noqa: E402
 from paper_1201_3972_b200.scene import CONFIGS, generate  # noqa: E402
 
-CASES = [("c1", 1), ("c2", 1), ("c2", 2), ("c3", 1), ("c4", 1), ("c5", 1)]
+CASES = [("c1", 1, "fnr"), ("c2", 1, "fnr"), ("c2", 2, "fnr"), ("c3", 1, "fnr"), ("c4", 1, "fnr"), ("c5", 1, "fnr"),
+         ("c1", 1, "mf"), ("c2", 1, "mf"), ("c3", 1, "mf"), ("c4", 1, "mf"), ("c5", 1, "mf")]
 
 
 def main() -> None:
     threads = len(os.sched_getaffinity(0))
     out = {}
-    for name, passes in CASES:
+    cache = {}
+    for name, passes, method in CASES:
         cfg = CONFIGS[name]
         t0 = time.perf_counter()
-        img = generate(cfg)
-        res, st = oracle.run_filter_c(img, cfg.k, "fnr", passes, threads=threads)
-        out[f"{name}_p{passes}"] = {
-            "config": name, "k": cfg.k, "passes": passes, "shape": list(img.shape), "dtype": str(img.dtype),
+        img = cache[name] if name in cache else generate(cfg)
+        cache = {name: img}
+        res, st = oracle.run_filter_c(img, cfg.k, method, passes, threads=threads)
+        key = f"{name}_{method}_p{passes}"
+        out[key] = {
+            "config": name, "k": cfg.k, "method": method, "passes": passes, "shape": list(img.shape),
+            "dtype": str(img.dtype),
             "input_sha256": hashlib.sha256(img.tobytes()).hexdigest(),
             "output_sha256": hashlib.sha256(res.tobytes()).hexdigest(),
             "stats": [st.minmax_scans, st.sorts, st.replacements, st.detected, st.passes],
         }
-        print(name, passes, out[f"{name}_p{passes}"]["stats"], f"{time.perf_counter() - t0:.1f} s", flush=True)
+        print(key, out[key]["stats"], f"{time.perf_counter() - t0:.1f} s", flush=True)
     with open(os.path.join(HERE, "full_configs.json"), "w") as fh:
         json.dump(out, fh, indent=1)
 

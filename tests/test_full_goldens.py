@@ -1,7 +1,7 @@
 """Full-size BASELINE configs vs full-size goldens (tests/golden/full_configs.json, made by
 tests/golden/make_full_goldens.py from the oracle): sha256 of the whole output and the
-FilterStats counters, through the device path and (c2, c4) the host path with the sparse
-result return. The input sha256 is checked first, so a scene-generator drift cannot pass
+FilterStats counters (FNR and MF), through the device path and (c2, c4 FNR) the host path
+with the sparse result return. The input sha256 is checked first, so a scene-generator drift cannot pass
 as a filter mismatch."""
 
 import hashlib
@@ -37,13 +37,14 @@ def test_full_size_config_matches_golden(cuda_ok, key):
     assert list(img.shape) == g["shape"] and _sha(img) == g["input_sha256"]
     u16 = img.dtype == np.uint16
     t = torch.from_numpy(img.view(np.int16) if u16 else img).cuda()
-    out, st = P.run_filter(t.view(torch.uint16) if u16 else t, P.WindowSpec(g["k"]), "fnr", g["passes"])
+    method = g.get("method", "fnr")
+    out, st = P.run_filter(t.view(torch.uint16) if u16 else t, P.WindowSpec(g["k"]), method, g["passes"])
     host = (out.view(torch.int16) if u16 else out).cpu().numpy()
     host = host.view(np.uint16) if u16 else host
     assert _sha(host) == g["output_sha256"], key
     assert [st.minmax_scans, st.sorts, st.replacements, st.detected, st.passes] == g["stats"], key
     del t, out
-    if g["config"] in ("c2", "c4"):  # host buffers: pipelined copies + the sparse result return
-        hout, hst = P.run_filter(img, P.WindowSpec(g["k"]), "fnr", g["passes"])
+    if g["config"] in ("c2", "c4") and method == "fnr":  # host buffers: pipelined copies + sparse return
+        hout, hst = P.run_filter(img, P.WindowSpec(g["k"]), method, g["passes"])
         assert _sha(hout) == g["output_sha256"], key
         assert [hst.minmax_scans, hst.sorts, hst.replacements, hst.detected, hst.passes] == g["stats"], key
