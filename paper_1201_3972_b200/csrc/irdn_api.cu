@@ -546,6 +546,37 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
     par_copy(h_out + chunk_off(chunks[i]), stage_out(i), (size_t)chunk_cnt(chunks[i]) * sizeof(T));
     return IRDN_OK;
   };
+  auto us = [&] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(); };
+  // Sparse return: rebuild chunk i on the host from h_in and the chunk's region.
+  const int nt = copy_threads();
+  double delta_ratio = 0.0;
+  size_t decoded = 0;
+  auto decode_chunk = [&](size_t i) -> int {
+    if (i == full_chunk) {  // came back by a full copy (synchronised with s_d2h at the end)
+      d2h_bytes += (uint64_t)chunk_cnt(chunks[i]) * sizeof(T);
+      return IRDN_OK;
+    }
+    IRDN_CUDA(cudaEventSynchronize(ev_done[i]));
+    if (trace) fprintf(stderr, "[irdn]   chunk %zu ready %.1f us", i, us());
+    const int64_t off = chunk_off(chunks[i]), cnt = chunk_cnt(chunks[i]);
+    uint8_t* src = ws.delta_h + delta_off[i];
+    const int64_t total = *reinterpret_cast<const uint32_t*>(src), budget = delta_budget(cnt);
+    if (total > budget) {  // more changed pixels than budgeted: fetch the rest of the values
+      const int64_t vo = delta::values_offset(cnt) + budget * (int64_t)sizeof(T);
+      const size_t extra = (size_t)(total - budget) * sizeof(T);
+      IRDN_CUDA(cudaMemcpyAsync(src + vo, ws.delta_d + delta_off[i] + vo, extra, cudaMemcpyDeviceToHost,
+                                ws.s_d2h));
+      IRDN_CUDA(cudaStreamSynchronize(ws.s_d2h));
+      d2h_bytes += extra;
+    }
+    delta_ratio = std::max(delta_ratio, (double)total / (double)cnt);
+    if constexpr (sizeof(T) == 1)
+      irdn_delta_decode_host_u8(src, h_in + off, h_out + off, cnt, nt, 1);
+    else
+      irdn_delta_decode_host_u16(src, h_in + off, h_out + off, cnt, nt, 1);
+    if (trace) fprintf(stderr, " decoded %.1f us (%lld px, %lld changed)\n", us(), (long long)cnt, (long long)total);
+    return IRDN_OK;
+  };
   // H2D: each chunk's own rows (row mode: strips, in order).
   if (!staged_in) {
     for (size_t i = 0; i < chunks.size(); ++i) {
@@ -647,38 +678,11 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   if (staged_out)
     for (size_t i = drained; i < chunks.size(); ++i)
       if ((rc = drain_out(i))) return rc;
-  auto us = [&] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(); };
   if (trace) fprintf(stderr, "[irdn] %zu chunks enqueued at %.1f us\n", chunks.size(), us());
   if (use_delta) {
-    const int nt = copy_threads();
-    double ratio = 0.0;
-    for (size_t i = 0; i < chunks.size(); ++i) {
-      if (i == full_chunk) {  // came back by a full copy (synchronised with s_d2h below)
-        d2h_bytes += (uint64_t)chunk_cnt(chunks[i]) * sizeof(T);
-        continue;
-      }
-      IRDN_CUDA(cudaEventSynchronize(ev_done[i]));
-      if (trace) fprintf(stderr, "[irdn]   chunk %zu ready %.1f us", i, us());
-      const int64_t off = chunk_off(chunks[i]), cnt = chunk_cnt(chunks[i]);
-      uint8_t* src = ws.delta_h + delta_off[i];
-      const int64_t total = *reinterpret_cast<const uint32_t*>(src), budget = delta_budget(cnt);
-      if (total > budget) {  // more changed pixels than budgeted: fetch the rest of the values
-        const int64_t vo = delta::values_offset(cnt) + budget * (int64_t)sizeof(T);
-        const size_t extra = (size_t)(total - budget) * sizeof(T);
-        IRDN_CUDA(cudaMemcpyAsync(src + vo, ws.delta_d + delta_off[i] + vo, extra, cudaMemcpyDeviceToHost,
-                                  ws.s_d2h));
-        IRDN_CUDA(cudaStreamSynchronize(ws.s_d2h));
-        d2h_bytes += extra;
-      }
-      ratio = std::max(ratio, (double)total / (double)cnt);
-      if constexpr (sizeof(T) == 1)
-        irdn_delta_decode_host_u8(src, h_in + off, h_out + off, cnt, nt, 1);
-      else
-        irdn_delta_decode_host_u16(src, h_in + off, h_out + off, cnt, nt, 1);
-      if (trace)
-        fprintf(stderr, " decoded %.1f us (%lld px, %lld changed)\n", us(), (long long)cnt, (long long)total);
-    }
-    ws.delta_ratio = ratio;
+    for (; decoded < chunks.size(); ++decoded)
+      if ((rc = decode_chunk(decoded))) return rc;
+    ws.delta_ratio = delta_ratio;
   } else {
     d2h_bytes += nbytes;
   }
