@@ -264,6 +264,14 @@ static int run_device(const T* d_in, T* d_out, T* d_tmp, int64_t batch, int64_t 
 
 // ---------------------------------------------------------------------------
 // Host-buffer run_filter with copy/compute pipelining.
+//
+// The batch is cut into ~8 MB chunks of whole frames (row strips for one large frame).
+// Per chunk: H2D on s_h2d (from pinned staging slots when the caller's buffer is
+// pageable), the passes on s_comp once its H2D event fires, then the result back on s_d2h:
+// either a full D2H copy, or — FNR on 16-bit frames — the sparse return (delta.cuh:
+// encode + one DMA of counts, masks and a value budget; the host rebuilds the chunk from
+// its own input, delta_host.cpp), with the last chunk split between the two. The
+// counters come back last (FilterStats accounting: filters.py:121-126).
 // ---------------------------------------------------------------------------
 struct DeviceWorkspace {
   std::mutex mu;
