@@ -178,7 +178,8 @@ IRDN_API int irdn_sq_err_sum_u16(const uint16_t* d_a, const uint16_t* d_b, int64
 IRDN_API int32_t irdn_set_multipass(int32_t on);
 
 /*
- * Result return of irdn_run_filter_*: 0 = auto (sparse for FNR on u16 frames, else full copy),
+ * Result return of irdn_run_filter_*: 0 = auto (sparse for FNR on u16 frames from a pinned
+ * input with >= 6 host threads per GPU process, else full copy),
  * 1 = full device->host copy of the output, 2 = sparse. Sparse: the device sends only
  * the output pixels that differ from the input (a per-4096-pixel count, a change
  * bit mask and the packed changed values, written by the encode kernel into mapped

@@ -489,8 +489,11 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   // about what the D2H saves (c3 2.06 -> 1.98 ms, but c5 31.8 -> 37.4 ms, c1 0.050 -> 0.067 ms)
   // (and only with >= 6 host threads for the rebuild: ~13 GB/s per thread, the full copy's
   // extra cost over the H2D is ~0.2-0.4 ms per 42 MB)
+  // (and only for a pinned input: with a pageable one the host threads are busy staging it,
+  // and the full copy wins — pageable c2 1.42-1.46 vs 1.46-1.59 ms, c4 4.12 vs 5.1-5.7 ms)
+  const bool in_pinned = is_pinned(h_in);
   const bool use_delta = g_host_return == 2 || (g_host_return == 0 && method == IRDN_METHOD_FNR &&
-                                                 sizeof(T) == 2 && copy_threads() >= 6);
+                                                 sizeof(T) == 2 && copy_threads() >= 6 && in_pinned);
   // Sparse return: the last chunk is rebuilt on the host after everything else has landed,
   // so its second half comes back by a plain D2H copy into the (pinned) caller buffer
   // instead, while the host rebuilds the first half (IRDN_SPLIT_LAST=0 disables).
@@ -541,7 +544,7 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
     return std::min<int64_t>(n, (int64_t)((double)n * ws.delta_ratio * 1.15) + 2 * delta::BLK);
   };
   uint64_t d2h_bytes = 16;  // the counters
-  const bool staged_in = !is_pinned(h_in), staged_out = !use_delta && !is_pinned(h_out);
+  const bool staged_in = !in_pinned, staged_out = !use_delta && !is_pinned(h_out);
   const bool staged = staged_in || staged_out;
   int64_t max_cnt = 0;
   for (const Chunk& c : chunks) max_cnt = std::max(max_cnt, chunk_cnt(c));
