@@ -210,3 +210,43 @@ def test_sparse_return_budget_overflow():
         assert wst[2] > 8 * 4096  # far more changed pixels than the flat call's budget
     finally:
         _native.set_host_return(prev)
+
+
+@pytest.mark.gpu
+def test_sparse_return_concurrent_pinned_calls():
+    """Host-buffer calls with pinned buffers (auto mode = sparse return for u16 FNR) from
+    several threads at once: the per-device workspace lock serialises them, results match."""
+    import threading
+
+    import torch
+
+    from oracle import oracle
+    from paper_1201_3972_b200.scene import CONFIGS, generate
+
+    lib = _native.load_lib()
+    cfg = CONFIGS["c2"].with_shape(height=256, width=320)
+    imgs = [generate(cfg, frame0=6 * i, nframes=6) for i in range(4)]
+    want = [oracle.run_filter_c(im, 5, "fnr", 1, threads=4) for im in imgs]
+    got, errs = [None] * len(imgs), []
+
+    def worker(i):
+        try:
+            hin = torch.from_numpy(imgs[i].view(np.int16)).pin_memory()
+            hout = torch.empty_like(hin).pin_memory()
+            st = _native.IrdnStats()
+            B, H, W = imgs[i].shape
+            _native.check(lib.irdn_run_filter_u16(hin.data_ptr(), hout.data_ptr(), B, H, W, 5, 0, 1, 0,
+                                                  ctypes.byref(st)))
+            got[i] = (hout.numpy().view(np.uint16).copy(), [st.minmax_scans, st.sorts, st.replacements,
+                                                            st.detected, st.passes])
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(len(imgs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for (w, wst), (g, gst) in zip(want, got):
+        assert np.array_equal(g, w) and gst == list(wst.counters())
