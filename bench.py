@@ -1,31 +1,38 @@
 #!/usr/bin/env python
-"""FNR filter benchmark: Mpix/s filtered (detect + median) on B200, BASELINE.json metric.
+"""FNR filter benchmark: Mpix/s filtered (detect+median) on B200, BASELINE.json metric.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl b200|reference]
 
 One "step" is one filter pass (method "fnr", passes=1 — the run_filter default,
-filters.py:83) over one batch of the workload. The default workload is
-BASELINE.json configs[1] (c2: 64 x 640x512 uint16 14-bit frames, 5x5 window);
-`--config c1..c5` selects another BASELINE config. For N > 1 (torchrun, one
-rank per GPU) every rank filters its own batch of further frames of the same
-seeded stream (frame sharding, no data-path collective: scaling "weak").
+filters.py:83) over the BASELINE workload. BASELINE.json's metric names no config, so
+the default workload is the largest single-GPU config, c5 (4096 x 640x480 u8 video
+frames, 3x3 window); `--config c1..c4` selects another one.
 
-Timing: W untimed warm-up steps, then K steps bracketed by barrier +
-synchronize, CUDA events on the launching stream, max over ranks. Steps
-rotate over R distinct input/output batches whose total size exceeds 2x the
-126 MB L2, so every step reads its input from HBM. Launches are replayed
-through a CUDA graph of R launches (the kernel count is unchanged).
+Multi-GPU (torchrun, one rank per GPU): the BASELINE workload is SPLIT
+across the ranks — c2 / c3 / c5 by frames (B/N contiguous frames per rank, the
+reference's band bounds), c4 by row strips (8192/N rows plus an r-row halo on each side,
+clamped against the global frame through irdn_filter_strip_*), strong scaling; c1 (one
+512x512 frame) runs as replicas (weak scaling). No data-path collective: the filter
+shards are independent; outputs stay sharded, and one gather of every shard to rank 0
+is timed separately (`gather`).
 
-The JSON line also carries: `roofline` (dominant kernel, algorithmic bytes
-2*sizeof(pixel) per pixel vs the measured HBM copy peak), `cpu_baseline`
-(the C restatement of the reference algorithm, 1 core, bounded sample), `e2e`
-(the same metric through the C-ABI host entry irdn_run_filter_* with pinned
-host buffers, H2D + D2H inside the timed region), `gpu_launches`, `clocks`.
+Timing: W untimed warm-up steps, then K steps bracketed by barrier + synchronize, CUDA
+events on the launching stream, max over ranks. Every step reads inputs larger than
+2x the 126 MB L2 (rotating distinct buffers when one batch is smaller). Launches are
+replayed through a CUDA graph (the kernel count is unchanged).
 
-`--impl reference` times the reference algorithm's CPU implementation — the
-oracle port (oracle/fnr_oracle.c: introsort medians, row-band threads), with
-every host thread — on the same config and metric. The reference itself is
-pure Python (irdenoise) and cannot be compiled.
+The JSON line also carries `roofline` (dominant kernel: algorithmic bytes 2*sizeof(pixel)
+per pixel vs the measured HBM copy peak, plus the ALU / issue floors from the committed
+ncu capture and the static min/max instruction count of the selection method),
+`cpu_baseline` (the C restatement of the reference algorithm, 1 core, bounded sample),
+`e2e` (the same metric through the C ABI with pinned host buffers, H2D + D2H inside the
+timed region), `gpu_launches` and `clocks`.
+
+`--impl reference` times the reference algorithm's CPU implementation — the oracle port
+(oracle/fnr_oracle.c: introsort medians, row-band threads) on every host thread — on the
+same config and metric; its input comes from the oracle library (no product library is
+loaded). When the unmodified reference package is installed in baseline/_ref, its own
+`run_filter` is timed beside it on a bounded sample (`python_reference`).
 """
 
 from __future__ import annotations
@@ -48,6 +55,8 @@ import numpy as np  # noqa: E402
 METRIC = "Mpix/s filtered (detect+median)"
 L2_BYTES = 126 * 1024 * 1024
 FALLBACK_HBM_GBS = 6650.0
+SM_COUNT, SM_MHZ = 148, 1965.0
+DATA = "synthetic (seeded IR scenes with the BASELINE.json shapes and noise models, DESIGN.md §5)"
 
 
 def parse():
@@ -55,10 +64,12 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="CPU-baseline sample budget (seconds of single-core oracle work)")
+    ap.add_argument("--ref-seconds", type=float, default=4.0,
+                    help="python_reference sample budget per step (reference arm)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
@@ -73,12 +84,87 @@ def parse():
 
 
 def default_steps(cfg) -> int:
-    # aim for a timed region of ~0.5-1 s so clocks can be sampled under load
-    return {"c1": 20000, "c2": 20000, "c3": 2000, "c4": 1000, "c5": 500}[cfg.name]
+    # aim for a timed region of ~0.4-1 s so clocks can be sampled under load
+    return {"c1": 20000, "c2": 20000, "c3": 2000, "c4": 2000, "c5": 600}[cfg.name]
 
 
-def workload_desc(cfg) -> str:
-    return f"{cfg.name}: {cfg.description}"
+# ---------------------------------------------------------------------------
+# Work split and the config block both arms report
+# ---------------------------------------------------------------------------
+def band_bounds(n: int, parts: int) -> list[int]:
+    """The reference's row-band bounds n*i//parts (filters.py:116)."""
+    return [n * i // parts for i in range(parts + 1)]
+
+
+def rank_share(cfg, world: int, rank: int) -> dict:
+    """What `rank` filters: a frame range, a row strip (+ halo), or a replica of the workload."""
+    if world == 1 or cfg.name == "c1":
+        return {"kind": "frames", "f0": 0, "f1": cfg.frames, "replica": world > 1}
+    if cfg.frames > 1:
+        b = band_bounds(cfg.frames, world)
+        return {"kind": "frames", "f0": b[rank], "f1": b[rank + 1], "replica": False}
+    b = band_bounds(cfg.height, world)
+    r = cfg.k // 2
+    y0, y1 = b[rank], b[rank + 1]
+    return {"kind": "rows", "y0": y0, "y1": y1, "in0": max(0, y0 - r), "in1": min(cfg.height, y1 + r),
+            "replica": False}
+
+
+def parallelism(cfg, world: int) -> str:
+    if world == 1:
+        return "1 GPU"
+    if cfg.name == "c1":
+        return f"replicas x{world} (one 512x512 frame per GPU; SURVEY.md §8e: replicas only)"
+    if cfg.frames > 1:
+        return f"frame-sharded over {world} GPUs ({cfg.frames} frames split {cfg.frames}/{world})"
+    return f"row strips over {world} GPUs ({cfg.height}/{world} rows + {cfg.k // 2}-row halos, global clamp)"
+
+
+def scaling_kind(cfg, world: int) -> str:
+    return "weak" if (cfg.name == "c1" and world > 1) else "strong"
+
+
+def config_block(cfg, world: int, passes: int) -> dict:
+    """Identical in both arms (the driver compares the arms' config)."""
+    return {"workload": f"{cfg.name}: {cfg.description}", "frames": cfg.frames, "height": cfg.height,
+            "width": cfg.width, "dtype": cfg.dtype, "k": cfg.k, "method": "fnr", "passes": passes,
+            "parallelism": parallelism(cfg, world)}
+
+
+def job_pixels(cfg, world: int) -> int:
+    """Pixels of one step summed over all ranks (replicas count once per rank)."""
+    return cfg.frames * cfg.height * cfg.width * (world if cfg.name == "c1" else 1)
+
+
+# ---------------------------------------------------------------------------
+# Static selection-method op counts (SURVEY.md §8d anti-gaming guard)
+# ---------------------------------------------------------------------------
+# Packed min/max instructions (VIMNMX / VIMNMX3 .U16x2, two pixels each) per two output
+# pixels, from the kernels' static schedule:
+#   dense 3x3 (fnr_k3.cuh, 16 output columns + 2 halo columns per thread):
+#     column sort 2 x 18/16, window min/max of column lows/highs 4, median of the three
+#     column middles 3 (sorted shared pair + clamp), final median-of-3 2
+#   warp kernel k = 5..11 (fnr_warp.cuh, 64 x 32 tiles, pixel pairs): detector
+#     (K-1)(1 + 2r/32) horizontal + (K-1) vertical + 1 flag test per pair, plus the median
+#     network for two flagged pixels (select_nets.cuh) times the detected fraction.
+NET_INSTR_PER_PAIR = {3: 30, 5: 172, 7: 514, 9: None, 11: 1833}
+
+
+def static_ops(cfg, detected_fraction: float) -> dict:
+    if cfg.k == 3 and cfg.dtype == "u8":
+        per_pair = 2 * 18 / 16 + 4 + 3 + 2
+        return {"method": "dense sorted-columns 3x3 median + extremum detector (every pixel)",
+                "minmax_instr_per_px": round(per_pair / 2, 3),
+                "minmax_lane_ops_per_px": round(per_pair, 3),
+                "note": "VIMNMX(3).U16x2 instructions per pixel (each covers 2 pixels); lane ops per pixel"}
+    K, r = cfg.k, cfg.k // 2
+    det = (K - 1) * (1 + 2 * r / 32) + (K - 1) + 1
+    net = NET_INSTR_PER_PAIR.get(K)
+    per_pair = det + (net or 0) * detected_fraction
+    return {"method": f"separable {K}x{K} extremum detector on every pixel pair + generated selection "
+                      f"network on the flagged pairs ({net} instructions per two medians)",
+            "minmax_instr_per_px": round(per_pair / 2, 3), "minmax_lane_ops_per_px": round(per_pair, 3),
+            "detected_fraction": round(detected_fraction, 4)}
 
 
 def read_peaks():
@@ -91,32 +177,14 @@ def read_peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def read_profile_traffic(cfg_name: str):
-    """dram bytes per launch of the dominant kernel from a committed ncu --set full capture."""
+def read_profile(cfg_name: str) -> dict:
+    """Per-launch figures of the dominant kernel from the committed ncu capture."""
     path = os.path.join(REPO, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
-            d = json.load(fh)
-        e = d.get(cfg_name) or {}
-        return e.get("dram_bytes_per_launch"), e
+            return json.load(fh).get(cfg_name) or {}
     except Exception:
-        return None, {}
-
-
-def read_alu_floor(cfg_name: str):
-    """ALU-pipe lane-ops per pixel of the dominant kernel (tools/prof/alu_floor.py output)."""
-    import glob
-
-    paths = sorted(glob.glob(os.path.join(REPO, "profiles", "alu_floor_*.json")))
-    for path in reversed(paths):  # newest capture tag first
-        try:
-            for row in json.load(open(path)):
-                if row["config"] == cfg_name:
-                    return dict(row, source=os.path.relpath(path, REPO) +
-                                " (ALU opcodes x 32 lanes from the ncu SASS mix; 64 lanes/clk/SM measured)")
-        except Exception:
-            continue
-    return None
+        return {}
 
 
 class ClockSampler:
@@ -179,10 +247,10 @@ class ClockSampler:
 _BACKEND = None
 
 
-def dist_setup(n_gpus: int):
-    """One rank per GPU (torchrun). NCCL carries the barrier / max-over-ranks timing; if
-    fewer GPUs than ranks are visible (a code-path check on a 1-GPU box) ranks share GPUs
-    and the control plane falls back to gloo. No data-path collective either way."""
+def dist_setup():
+    """One rank per GPU (torchrun). NCCL carries the barrier / max-over-ranks timing and the
+    separately timed gather; if fewer GPUs than ranks are visible (a code-path check on a
+    1-GPU box) ranks share the GPU and the control plane falls back to gloo."""
     global _BACKEND
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -209,51 +277,110 @@ def _max_over_ranks(value: float, dev) -> float:
     return float(t.item())
 
 
+def _gather_sum(values: list[int], dev) -> list[int]:
+    """Sum small integer vectors on the host: all_gather (no reduction collective), then add."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(values, dtype=torch.int64, device=dev if _BACKEND == "nccl" else "cpu")
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t)
+    return [int(x) for x in torch.stack(parts).cpu().sum(0).tolist()]
+
+
 # ---------------------------------------------------------------------------
 # CPU legs (oracle = the reference algorithm restated in C; test/baseline only)
 # ---------------------------------------------------------------------------
-def cpu_sample_run(cfg, frames: np.ndarray, threads: int, budget_s: float, full_frame=None):
-    """Run the oracle port over a bounded sample; returns (pixels, seconds, description)."""
+def cpu_sample_run(cfg, frames: np.ndarray, budget_s: float):
+    """One-thread oracle port over a bounded sample; returns (pixels, seconds, description)."""
     from oracle import oracle
 
     t0 = time.perf_counter()
     px = 0
-    if cfg.frames == 1 and cfg.height * cfg.width > (4 << 20):
-        # one huge frame (c4): row bands of the full frame, clamped against the frame
-        frame = full_frame if full_frame is not None else frames[0]
-        band = 16
-        y = 0
-        bands = 0
-        while time.perf_counter() - t0 < budget_s and y < cfg.height:
-            oracle.filter_rows_c(frame, cfg.k, y, min(cfg.height, y + band)) if threads == 1 else \
-                _threaded_rows(frame, cfg.k, y, min(cfg.height, y + band * threads), threads)
-            rows = band if threads == 1 else band * threads
-            px += min(rows, cfg.height - y) * cfg.width
-            y += rows
-            bands += 1
+    if frames.shape[0] == 1 and cfg.height * cfg.width > (4 << 20):
+        frame = frames[0]
+        y, band = 0, 16
+        while time.perf_counter() - t0 < budget_s and y < frame.shape[0]:
+            oracle.filter_rows_c(frame, cfg.k, y, min(frame.shape[0], y + band))
+            px += min(band, frame.shape[0] - y) * cfg.width
+            y += band
         desc = f"{px // cfg.width} rows x {cfg.width} of the {cfg.height}x{cfg.width} frame (row bands)"
     else:
         n = 0
         while time.perf_counter() - t0 < budget_s and n < frames.shape[0]:
-            oracle.run_filter_c(frames[n], cfg.k, "fnr", 1, threads=threads)
+            oracle.run_filter_c(frames[n], cfg.k, "fnr", 1, threads=1)
             px += cfg.height * cfg.width
             n += 1
         desc = f"{n} frame(s) of {cfg.height}x{cfg.width} {cfg.dtype}"
     return px, time.perf_counter() - t0, desc
 
 
-def _threaded_rows(frame, k, y0, y1, threads):
-    from oracle import oracle
+def _pyref_worker(args):
+    """One process of the python_reference leg: the UNMODIFIED reference package
+    (baseline/_ref) filtering a crop of `rows` output rows with r context rows."""
+    ref_path, crop, dtype, k, r_top, rows = args
+    sys.path.insert(0, ref_path)
+    import irdenoise as ird  # noqa: F401  (the reference, pip-installed into baseline/_ref)
+    from irdenoise import image as rimg
+    from irdenoise import filters as rfil
+    from irdenoise import sorting as rsort
 
-    # oracle_run_filter splits a frame into row bands itself; for a row range use bands per thread
-    ts = []
-    step = max(1, (y1 - y0 + threads - 1) // threads)
-    for a in range(y0, y1, step):
-        t = threading.Thread(target=oracle.filter_rows_c, args=(frame, k, a, min(y1, a + step)))
-        t.start()
-        ts.append(t)
-    for t in ts:
-        t.join()
+    h, w = crop.shape
+    t0 = time.perf_counter()
+    if dtype == "u8":
+        img = rimg.GrayImage(w, h, bytearray(crop.tobytes()))
+        rfil.run_filter(img, rimg.WindowSpec(k), "fnr", 1, threads=1)
+    else:
+        # u16: the reference's dtype-agnostic per-window API (SURVEY.md §8c u16 oracle)
+        class Img:
+            pass
+        from array import array
+        im = Img()
+        im.width, im.height, im.pixels = w, h, array("H", crop.tobytes())
+        spec = rimg.WindowSpec(k)
+        st = rfil.FilterStats()
+        for y in range(r_top, r_top + rows):
+            for x in range(w):
+                win = rimg.extract_window(im, x, y, spec)
+                if rfil.classify_pixel(win, rfil.window_extrema(win, st)):
+                    rsort.median_of(win.values)
+    return rows * w, time.perf_counter() - t0
+
+
+def python_reference_leg(cfg, frames: np.ndarray, budget_s: float):
+    """Time the unmodified reference (baseline/_ref) with one process per host core on a
+    bounded sample: each worker filters a crop of the workload's frames (whole frames for
+    u8 run_filter, rows + r context rows for the u16 per-window path)."""
+    ref_path = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_path, "irdenoise")):
+        return {"unavailable": "reference not installed in baseline/_ref (DESIGN.md §3)"}
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    r = cfg.k // 2
+    # per-core rate (SURVEY §6): ~0.3 Mpix/s at k=3 down to ~0.015 at k=11 (u16); size crops for the budget
+    rate = {3: 0.28e6, 5: 0.07e6, 7: 0.08e6, 11: 0.015e6}.get(cfg.k, 0.05e6)
+    rows = max(1, min(cfg.height, int(rate * budget_s * 0.6 / cfg.width)))
+    jobs = []
+    for i in range(cores):
+        f = frames[i % frames.shape[0]]
+        y0 = (i * 37) % max(1, cfg.height - rows + 1)
+        a, b = max(0, y0 - r), min(cfg.height, y0 + rows + r)
+        jobs.append((ref_path, np.ascontiguousarray(f[a:b]), cfg.dtype, cfg.k, y0 - a,
+                     rows if cfg.dtype != "u8" else b - a))
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_pyref_worker, jobs)
+    wall = time.perf_counter() - t0
+    px = sum(p for p, _ in res)
+    per_proc = statistics.median(p / s for p, s in res)
+    return {"value": round(px / wall / 1e6, 4), "unit": "Mpix/s", "cores": cores,
+            "per_core_value": round(per_proc / 1e6, 4),
+            "sample": f"{cores} processes x {rows if cfg.dtype != 'u8' else 'crop of'} rows x {cfg.width} "
+                      f"({'run_filter on GrayImage crops' if cfg.dtype == 'u8' else 'per-window API'}), "
+                      f"wall {wall:.1f} s incl. process start",
+            "source": "unmodified irdenoise 0.1.0 from baseline/_ref (pip install --target)"}
 
 
 def run_reference_arm(args, cfg, rank: int, world: int):
@@ -262,22 +389,20 @@ def run_reference_arm(args, cfg, rank: int, world: int):
     from oracle import oracle
     from paper_1201_3972_b200.scene import generate
 
-    oracle.lib()
+    olib = oracle.lib()  # oracle port + the same seeded scene source; no product library
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     steps = args.steps if args.steps is not None else 5
-    # sample: whole frames for batch configs, row bands of the frame for c4
     if cfg.frames == 1 and cfg.height * cfg.width > (4 << 20):
-        frame = generate(cfg, nframes=1)[0]
+        frame = generate(cfg, nframes=1, lib=olib)[0]
         rows = 64 * threads
+        sample_frames = frame[None, : rows + cfg.k]
 
         def step():
-            from oracle import oracle as o
-
             ts = []
             per = rows // threads
             for i in range(threads):
                 a = i * per
-                t = threading.Thread(target=o.filter_rows_c, args=(frame, cfg.k, a, a + per))
+                t = threading.Thread(target=oracle.filter_rows_c, args=(frame, cfg.k, a, a + per))
                 t.start()
                 ts.append(t)
             for t in ts:
@@ -285,13 +410,13 @@ def run_reference_arm(args, cfg, rank: int, world: int):
             return rows * cfg.width
         sample = f"{rows} rows x {cfg.width} of the {cfg.height}x{cfg.width} frame per step, {threads} threads"
     else:
-        nfr = 1
-        probe = generate(cfg, nframes=1)
+        probe = generate(cfg, nframes=1, lib=olib)
         t0 = time.perf_counter()
         oracle.run_filter_c(probe, cfg.k, "fnr", 1, threads=threads)
         dt = time.perf_counter() - t0
         nfr = int(max(1, min(cfg.frames, math.ceil(1.0 / max(dt, 1e-4)))))
-        frames = generate(cfg, nframes=nfr)
+        frames = generate(cfg, nframes=nfr, lib=olib)
+        sample_frames = frames
 
         def step():
             oracle.run_filter_c(frames, cfg.k, "fnr", 1, threads=threads)
@@ -305,16 +430,18 @@ def run_reference_arm(args, cfg, rank: int, world: int):
         px += step()
     dt = time.perf_counter() - t0
     value = px / dt / 1e6
+    pyref = python_reference_leg(cfg, sample_frames, args.ref_seconds)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Mpix/s",
         "n_gpus": world, "steps": steps, "warmup": args.warmup,
-        "ms_per_step": round(dt / steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded IR scenes, DESIGN.md §5)",
-        "config": {"workload": workload_desc(cfg), "method": "fnr", "passes": 1, "k": cfg.k},
+        "ms_per_step": round(dt / steps * 1e3, 3), "higher_is_better": True, "scaling": scaling_kind(cfg, world),
+        "vs_baseline": None, "dtype": cfg.dtype, "data": DATA,
+        "config": config_block(cfg, world, 1),
         "cpu_baseline": {"value": round(value, 4), "unit": "Mpix/s", "cores": threads, "kind": "port",
                          "sample": sample,
                          "note": "oracle/fnr_oracle.c: C restatement of the reference's run_filter "
                                  "(introsort medians, row-band threads); the reference is pure Python"},
+        "python_reference": pyref,
         "e2e": {"value": round(value, 4), "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -337,35 +464,49 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
         lib.irdn_set_multipass(1)
     steps = args.steps if args.steps is not None else default_steps(cfg)
     warmup = max(3, args.warmup)
-    bpp = cfg.bytes_per_pixel
-    B, H, W = cfg.frames, cfg.height, cfg.width
-    batch_px = B * H * W
-    batch_bytes = batch_px * bpp
-
-    # this rank's batch: frames [rank*B, (rank+1)*B) of the seeded stream (c1/c4: replicas)
-    frame0 = rank * B if B > 1 else 0
-    host = generate(cfg, frame0=frame0, nframes=B)
-    h_in = torch.from_numpy(host).pin_memory() if bpp == 1 else \
-        torch.from_numpy(host.view(np.int16)).pin_memory()
-    d0 = h_in.to(dev, non_blocking=False)  # u16 pixels travel as int16 bit patterns
-    R = max(1, math.ceil(2 * L2_BYTES / (2 * batch_bytes)))
-    ins = [d0] + [d0.clone() for _ in range(R - 1)]
-    outs = [torch.empty_like(d0) for _ in range(R)]
-    counts = torch.zeros(2, dtype=torch.int64, device=dev)
-    fn = lib.irdn_filter_pass_u8 if bpp == 1 else lib.irdn_filter_pass_u16
-    dfn = lib.irdn_run_filter_device_u8 if bpp == 1 else lib.irdn_run_filter_device_u16
     passes = max(1, args.passes)
-    tmp = torch.empty_like(d0) if passes > 1 else None
+    share = rank_share(cfg, world, rank)
+    bpp = cfg.bytes_per_pixel
+    H, W = cfg.height, cfg.width
+    if share["kind"] == "frames":
+        B = share["f1"] - share["f0"]
+        host = generate(cfg, frame0=share["f0"], nframes=B)
+        out_rows = H
+        rank_px = B * H * W
+    else:
+        if passes > 1:
+            raise SystemExit("row strips (c4 at N > 1) are benchmarked with passes = 1")
+        B = 1
+        full = generate(cfg, nframes=1)
+        host = np.ascontiguousarray(full[:, share["in0"]:share["in1"]])
+        del full
+        out_rows = share["y1"] - share["y0"]
+        rank_px = out_rows * W
+    h_in = torch.from_numpy(host).pin_memory() if bpp == 1 else torch.from_numpy(host.view(np.int16)).pin_memory()
+    d0 = h_in.to(dev, non_blocking=False)  # u16 pixels travel as int16 bit patterns
+    in_bytes = d0.numel() * bpp
+    out_shape = (B, out_rows, W)
+    R = max(1, math.ceil(2 * L2_BYTES / (in_bytes + rank_px * bpp)))
+    ins = [d0] + [d0.clone() for _ in range(R - 1)]
+    outs = [torch.empty(out_shape, dtype=d0.dtype, device=dev) for _ in range(R)]
+    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    tmp = torch.empty_like(outs[0]) if passes > 1 else None
     stream = torch.cuda.Stream(dev)
     sptr = stream.cuda_stream
+    t = "u8" if bpp == 1 else "u16"
+    fpass = getattr(lib, f"irdn_filter_pass_{t}")
+    fdev = getattr(lib, f"irdn_run_filter_device_{t}")
+    fstrip = getattr(lib, f"irdn_filter_strip_{t}")
 
     def launch(i: int):
-        if passes == 1:
-            rc = fn(ins[i % R].data_ptr(), outs[i % R].data_ptr(), B, H, W, W, W, cfg.k, 0,
-                    counts.data_ptr(), sptr)
-        else:  # run_filter over device buffers: all passes in one multi-pass launch (via tmp)
-            rc = dfn(ins[i % R].data_ptr(), outs[i % R].data_ptr(), tmp.data_ptr(), B, H, W, cfg.k, 0, passes,
-                     counts.data_ptr(), sptr)
+        src, dst = ins[i % R].data_ptr(), outs[i % R].data_ptr()
+        if share["kind"] == "rows":
+            rc = fstrip(src, share["in0"], share["in1"] - share["in0"], dst, share["y0"], share["y1"], H, W, W, W,
+                        cfg.k, 0, counts.data_ptr(), sptr)
+        elif passes == 1:
+            rc = fpass(src, dst, B, H, W, W, W, cfg.k, 0, counts.data_ptr(), sptr)
+        else:  # run_filter over device buffers: passes back-to-back launches through tmp
+            rc = fdev(src, dst, tmp.data_ptr(), B, H, W, cfg.k, 0, passes, counts.data_ptr(), sptr)
         if rc != 0:
             _native.check(rc)
 
@@ -373,7 +514,6 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
         for i in range(warmup):
             launch(i)
     torch.cuda.synchronize(dev)
-    # kernel launches per step (1 for passes > 1 too: all passes run in one multi-pass launch)
     lib.irdn_reset_launch_count()
     with torch.cuda.stream(stream):
         launch(0)
@@ -420,18 +560,23 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
     sampler.stop()
     eager_launches = int(lib.irdn_launch_count())
     gpu_launches = ((steps // R) * R + (steps % R)) * per_step if graph is not None else eager_launches
-    elapsed_ms = ev0.elapsed_time(ev1)
+    rank_ms = ev0.elapsed_time(ev1)
+    elapsed_ms = rank_ms
+    det_rank = int(counts[0].item())
+    det_total = det_rank
     if world > 1:
-        import torch.distributed as dist
-
-        elapsed_ms = _max_over_ranks(elapsed_ms, dev)
-        dist.barrier()
-    det = int(counts[0].item())
+        elapsed_ms = _max_over_ranks(rank_ms, dev)
+        det_total = _gather_sum([det_rank], dev)[0]
     ms_per_step = elapsed_ms / steps
-    value = world * batch_px * passes * steps / (elapsed_ms * 1e-3) / 1e6
+    value = job_pixels(cfg, world) * passes * steps / (elapsed_ms * 1e-3) / 1e6
 
-    # dominant-kernel duration: per-launch CUDA events on the launching stream (separate pass)
-    per = []
+    # gather: every rank's output shard to rank 0 (outputs otherwise stay sharded), timed alone
+    gather = None
+    if world > 1:
+        gather = time_gather(outs[0], dev, rank, world, share, cfg)
+
+    # the dominant kernel: this rank's per-launch average over the timed region; isolated
+    # per-launch events (which defeat the programmatic-dependent-launch overlap) beside it
     nper = min(steps, 200)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nper)]
     with torch.cuda.stream(stream):
@@ -440,62 +585,165 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
             launch(i)
             evs[i][1].record(stream)
     torch.cuda.synchronize(dev)
-    per = [a.elapsed_time(b) / passes for a, b in evs]  # per filter launch, isolated by events
-    # the dominant kernel's average launch duration over the timed region: the region
-    # holds exactly steps x passes filter launches back to back (programmatic dependent
-    # launch overlaps each launch's ramp with the previous one's tail); the isolated
-    # per-launch figure (events around every launch defeat that overlap) is kept beside it
-    kernel_ms = elapsed_ms / (steps * passes)
+    per = [a.elapsed_time(b) / passes for a, b in evs]
+    kernel_ms = rank_ms / (steps * passes)
 
     peak, peak_src = read_peaks()
-    alg_bytes = batch_px * 2 * bpp
+    alg_bytes = rank_px * 2 * bpp
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
-    traffic, prof = read_profile_traffic(cfg.name)
+    prof = read_profile(cfg.name)
+    traffic = prof.get("dram_bytes_per_launch")
+    if traffic is not None and prof.get("pixels_per_launch"):
+        traffic = traffic * rank_px / prof["pixels_per_launch"]
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac": round(achieved / peak, 4), "traffic": round(traffic) if traffic else None,
                 "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": alg_bytes,
-                "bytes_per_pixel": 2 * bpp, "pixels_per_launch": batch_px,
+                "algorithmic_bytes_per_launch": alg_bytes, "bytes_per_pixel": 2 * bpp,
+                "pixels_per_launch": rank_px,
                 "kernel_ms": round(kernel_ms, 5),
-                "kernel_ms_source": "CUDA events over the timed region / filter launches in it",
+                "kernel_ms_source": "CUDA events on the launching stream over the timed region / filter launches",
                 "kernel_ms_isolated": round(statistics.mean(per), 5),
-                "kernel_ms_isolated_min": round(min(per), 5)}
-    if prof.get("alu"):
-        roofline["alu"] = {k: v for k, v in prof["alu"].items() if v is not None}
-    alu = read_alu_floor(cfg.name)
-    if alu:
-        # the binding roofline for every config (ALU floor > HBM floor): ALU-pipe lane-ops per
-        # pixel are a property of the kernel and the scene (counted from the ncu SASS mix of
-        # the committed capture), the time is this run's per-launch kernel time
-        ops = alu["alu_lane_ops_per_px"] * batch_px
-        peak_alu = 64 * 148 * 1.965e9
-        roofline.setdefault("alu", {}).update({
-            "lane_ops_per_px": round(alu["alu_lane_ops_per_px"], 2),
-            "achieved_Tops": round(ops / (kernel_ms * 1e-3) / 1e12, 3),
-            "peak_Tops": round(peak_alu / 1e12, 3),
-            "frac": round(ops / (kernel_ms * 1e-3) / peak_alu, 4),
-            "floor_us": round(ops / peak_alu * 1e6, 2),
-            "source": alu["source"]})
-        if "instr_per_px" in alu:
-            # issue roofline: every instruction needs an issue slot (4 per clk per SM)
-            instr = alu["instr_per_px"] * batch_px
-            peak_issue = 128 * 148 * 1.965e9
-            roofline["issue"] = {"instr_per_px": round(alu["instr_per_px"], 2),
-                                 "floor_us": round(instr / peak_issue * 1e6, 2),
-                                 "frac": round(instr / (kernel_ms * 1e-3) / peak_issue, 4),
-                                 "peak_Tinstr": round(peak_issue / 1e12, 3)}
+                "kernel_ms_isolated_min": round(min(per), 5),
+                "static_ops": static_ops(cfg, det_rank / max(1, rank_px * steps * passes))}
+    if prof.get("instr_per_px"):
+        # SM-side floors from the committed capture (instructions / ALU-pipe instructions per pixel)
+        ipp, app = prof["instr_per_px"], prof.get("alu_instr_per_px")
+        issue_peak = 128 * SM_COUNT * SM_MHZ * 1e6
+        alu_peak = 64 * SM_COUNT * SM_MHZ * 1e6
+        roofline["issue"] = {"instr_per_px": round(ipp, 2), "frac": round(ipp * rank_px / (kernel_ms * 1e-3) / issue_peak, 4),
+                             "floor_us": round(ipp * rank_px / issue_peak * 1e6, 2),
+                             "peak": "4 warp-instructions/clk/SM x 148 SMs x 1965 MHz"}
+        if app:
+            roofline["alu"] = {"alu_instr_per_px": round(app, 2),
+                               "frac": round(app * rank_px / (kernel_ms * 1e-3) / alu_peak, 4),
+                               "floor_us": round(app * rank_px / alu_peak * 1e6, 2),
+                               "peak": "2 warp-instructions/clk/SM (VIMNMX/PRMT/IADD3/LOP3, "
+                                       "profiles/pipe_probe_r02.txt) x 148 x 1965 MHz"}
+        roofline["profile"] = prof.get("source")
 
-    # e2e through the C-ABI host entry: pinned host in/out, H2D + filter + D2H each step
-    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(steps, 20 if batch_bytes > (256 << 20) else 50))
-    h_out = torch.empty_like(h_in).pin_memory()
-    st = _native.IrdnStats()
-    hfn = lib.irdn_run_filter_u8 if bpp == 1 else lib.irdn_run_filter_u16
-    for _ in range(2):
-        _native.check(hfn(h_in.data_ptr(), h_out.data_ptr(), B, H, W, cfg.k, 0, passes, local, ctypes.byref(st)))
+    e2e = run_e2e(args, cfg, lib, _native, h_in, outs[0], share, steps, dev, world, passes, local)
+    e2e_det = e2e.pop("_detected")
+    if e2e_det is not None and e2e_det * steps != det_rank:
+        raise AssertionError("counter mismatch between the device-resident and the host-buffer path")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle
+
+        oracle.lib()
+        px, secs, desc = cpu_sample_run(cfg, host, args.cpu_seconds)
+        cpu = {"value": round(px / secs / 1e6, 4), "unit": "Mpix/s", "cores": 1, "kind": "port",
+               "sample": desc + f" ({secs:.1f} s)",
+               "note": "oracle/fnr_oracle.c (reference algorithm restated in C: clamp gather, "
+                       "min/max detector, introsort median), single thread"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Mpix/s", "n_gpus": world,
+            "steps": steps, "warmup": warmup, "ms_per_step": round(ms_per_step, 5),
+            "higher_is_better": True, "scaling": scaling_kind(cfg, world), "vs_baseline": None,
+            "dtype": cfg.dtype, "data": DATA,
+            "config": config_block(cfg, world, passes),
+            "run": {"pixels_per_step": job_pixels(cfg, world), "rank0_share": share,
+                    "detected_per_step": det_total // steps,
+                    "l2": f"rotating {R} distinct in/out buffers ({(in_bytes + rank_px * bpp) * R / 1e6:.0f} MB > 2x L2)"
+                          if R > 1 else f"in+out {(in_bytes + rank_px * bpp) / 1e6:.0f} MB per step > 2x L2",
+                    "launch": "CUDA graph of R launches" if graph is not None else "eager",
+                    **({"multipass_launch": True} if args.multipass and passes > 1 else {}),
+                    "collective_backend": _BACKEND},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": gpu_launches * world, "clocks": sampler.summary(),
+        }
+        if gather is not None:
+            line["gather"] = gather
+        print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
         dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def time_gather(out, dev, rank: int, world: int, share: dict, cfg):
+    """One gather of every rank's output shard to rank 0 (P2P over NVLink through NCCL on a
+    multi-GPU node; through the host with the gloo fallback), timed on its own."""
+    import torch
+    import torch.distributed as dist
+
+    flat = out.reshape(-1)
+    n = torch.tensor([flat.numel()], dtype=torch.int64, device=dev if _BACKEND == "nccl" else "cpu")
+    sizes = [torch.empty_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(sizes)
+    send = flat if _BACKEND == "nccl" else flat.cpu()
+    if send.numel() < mx:
+        send = torch.cat([send, send.new_zeros(mx - send.numel())])
+    bufs = [torch.empty_like(send) for _ in range(world)] if rank == 0 else None
+    for _ in range(2):  # warm-up (connection setup)
+        dist.gather(send, bufs, dst=0)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t0 = time.perf_counter()
+    dist.gather(send, bufs, dst=0)
+    torch.cuda.synchronize(dev)
+    secs = _max_over_ranks(time.perf_counter() - t0, dev)
+    bytes_in = sum(sizes) * out.element_size()
+    return {"ms": round(secs * 1e3, 3), "bytes": bytes_in, "backend": _BACKEND,
+            "note": "outputs stay sharded during the filter; this is one gather to rank 0, "
+                    "not included in value"}
+
+
+def run_e2e(args, cfg, lib, _native, h_in, d_out_ref, share, steps, dev, world, passes, local):
+    """e2e: the same metric through the C ABI with pinned host buffers, H2D + D2H timed."""
+    import torch
+
+    bpp = cfg.bytes_per_pixel
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(steps, 10 if h_in.numel() * bpp > (256 << 20) else 40))
+    t = "u8" if bpp == 1 else "u16"
+    H, W = cfg.height, cfg.width
+    if share["kind"] == "rows":
+        # a row strip: H2D of the strip (+ halo rows), irdn_filter_strip_*, D2H of the owned rows
+        fstrip = getattr(lib, f"irdn_filter_strip_{t}")
+        rows = share["y1"] - share["y0"]
+        h_out = torch.empty((1, rows, W), dtype=h_in.dtype).pin_memory()
+        d_in = torch.empty_like(h_in, device=dev)
+        d_out = torch.empty((1, rows, W), dtype=h_in.dtype, device=dev)
+        counts = torch.zeros(2, dtype=torch.int64, device=dev)
+        s = torch.cuda.current_stream(dev)
+
+        def call():
+            d_in.copy_(h_in, non_blocking=True)
+            _native.check(fstrip(d_in.data_ptr(), share["in0"], share["in1"] - share["in0"], d_out.data_ptr(),
+                                 share["y0"], share["y1"], H, W, W, W, cfg.k, 0, counts.data_ptr(), s.cuda_stream))
+            h_out.copy_(d_out, non_blocking=True)
+            s.synchronize()
+        call()
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            call()
+        secs = time.perf_counter() - t0
+        if world > 1:
+            secs = _max_over_ranks(secs, dev)
+        if not torch.equal(h_out.to(dev), d_out_ref):
+            raise AssertionError("e2e strip output differs from the device-resident output")
+        return {"value": round(job_pixels(cfg, world) * e2e_steps / secs / 1e6, 3), "unit": "Mpix/s",
+                "h2d_bytes_per_step": h_in.numel() * bpp, "d2h_bytes_per_step": rows * W * bpp,
+                "steps": e2e_steps, "_detected": None,
+                "api": f"irdn_filter_strip_{t} (C ABI) between pinned host buffers; host wall clock"}
+
+    B = share["f1"] - share["f0"]
+    h_out = torch.empty_like(h_in).pin_memory()
+    st = _native.IrdnStats()
+    hfn = getattr(lib, f"irdn_run_filter_{t}")
+    for _ in range(2):
+        _native.check(hfn(h_in.data_ptr(), h_out.data_ptr(), B, H, W, cfg.k, 0, passes, local, ctypes.byref(st)))
+
     def e2e_run(mode: str):
         prev = _native.set_host_return(mode)
         try:
@@ -515,60 +763,22 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
             h2d, d2h = _native.last_transfer()
         finally:
             _native.set_host_return(prev)
-        # consistency: the e2e output equals the device-resident output
-        if not torch.equal(h_out.to(dev), outs[0]):
+        if passes == 1 and not torch.equal(h_out.to(dev), d_out_ref):
             raise AssertionError(f"e2e output ({mode} return) differs from the device-resident output")
-        return world * batch_px * passes * e2e_steps / secs / 1e6, h2d, d2h
+        return job_pixels(cfg, world) * passes * e2e_steps / secs / 1e6, h2d, d2h
 
     full_v, _, full_d2h = e2e_run("full")
     e2e_v, h2d, d2h = e2e_run("auto")
-    e2e = {"value": round(e2e_v, 3), "unit": "Mpix/s",
-           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "steps": e2e_steps,
-           "api": f"irdn_run_filter_{cfg.dtype} (C ABI, include/irdn.h) on pinned host buffers; "
-                  "host wall clock, call is synchronous",
-           "result_return": "sparse (changed pixels only, rebuilt on the host from its input; DESIGN.md §7.1)"
-                            if d2h < batch_bytes else "full D2H copy (auto mode: 8-bit frames, or < 6 host "
-                                                      "threads per GPU process; DESIGN.md §7.1)",
-           "full_copy": {"value": round(full_v, 3), "d2h_bytes_per_step": full_d2h}}
-    if st.detected * steps != det:
-        raise AssertionError(f"counter mismatch: {st.detected}*{steps} != {det}")
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import oracle
-
-        oracle.lib()
-        px, secs, desc = cpu_sample_run(cfg, host, 1, args.cpu_seconds)
-        cpu = {"value": round(px / secs / 1e6, 4), "unit": "Mpix/s", "cores": 1, "kind": "port",
-               "sample": desc + f" ({secs:.1f} s)",
-               "note": "oracle/fnr_oracle.c (reference algorithm restated in C: clamp gather, "
-                       "min/max detector, introsort median), single thread"}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": round(value, 3), "unit": "Mpix/s", "n_gpus": world,
-            "steps": steps, "warmup": warmup, "ms_per_step": round(ms_per_step, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
-            "data": "synthetic (seeded IR scenes, DESIGN.md §5)",
-            "config": {"workload": workload_desc(cfg), "frames_per_gpu": B, "height": H, "width": W,
-                       "k": cfg.k, "method": "fnr", "passes": passes,
-                       **({"multipass_launch": True} if args.multipass and passes > 1 else {}),
-                       "detected_per_step": det // steps,
-                       "l2": f"rotating {R} distinct in/out batch buffers "
-                             f"({2 * R * batch_bytes / 1e6:.0f} MB > 2x L2)" if R > 1 else
-                             f"in+out {2 * batch_bytes / 1e6:.0f} MB per step > 2x L2",
-                       "launch": "CUDA graph of R launches" if graph is not None else "eager",
-                       "parallelism": f"frame-sharded x{world}" if world > 1 else "1 GPU"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": gpu_launches, "clocks": sampler.summary(),
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.destroy_process_group()
-    return 0
+    batch_bytes = h_in.numel() * bpp
+    return {"value": round(e2e_v, 3), "unit": "Mpix/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+            "api": f"irdn_run_filter_{t} (C ABI, include/irdn.h) on pinned host buffers; "
+                   "host wall clock, call is synchronous",
+            "result_return": "sparse (changed pixels only, rebuilt on the host from its input; DESIGN.md §7.1)"
+                             if d2h < batch_bytes else "full D2H copy (auto mode: 8-bit frames, or < 6 host "
+                                                       "threads per GPU process; DESIGN.md §7.1)",
+            "full_copy": {"value": round(full_v, 3), "d2h_bytes_per_step": full_d2h},
+            "_detected": int(st.detected)}
 
 
 def main():
@@ -580,7 +790,7 @@ def main():
     from paper_1201_3972_b200.scene import CONFIGS
 
     cfg = CONFIGS[args.config]
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local = dist_setup()
     if args.impl == "reference":
         rc = run_reference_arm(args, cfg, rank, world)
         if world > 1:

@@ -29,6 +29,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle_fnr.so")
+# input preparation (seeded BASELINE scenes), linked into the oracle library as well
+SCENE_SRC = os.path.join(os.path.dirname(HERE), "paper_1201_3972_b200", "csrc", "scene.c")
 
 
 class OracleStats(ctypes.Structure):
@@ -66,8 +68,9 @@ def build() -> str:
 def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
-        src = os.path.join(HERE, "fnr_oracle.c")
-        if not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
+        srcs = [os.path.join(HERE, "fnr_oracle.c"), SCENE_SRC]
+        if not os.path.exists(LIB_PATH) or any(os.path.exists(f) and os.path.getmtime(LIB_PATH) <
+                                               os.path.getmtime(f) for f in srcs):
             build()
         l = ctypes.CDLL(LIB_PATH)
         vp, i64 = ctypes.c_void_p, ctypes.c_int64
@@ -87,6 +90,8 @@ def lib() -> ctypes.CDLL:
         l.oracle_inject_impulse.restype = ctypes.c_uint64
         l.oracle_sq_err_sum.argtypes = [vp, vp, ctypes.c_int, i64]
         l.oracle_sq_err_sum.restype = ctypes.c_uint64
+        l.scene_generate.restype = ctypes.c_int
+        l.scene_generate.argtypes = [vp, i64, i64, vp, ctypes.c_int32]
         _lib = l
     return _lib
 

@@ -148,27 +148,39 @@ inline int sm_count(int dev) {
   return cache[dev];
 }
 
-// Per-device pool of tile-scheduler slots ({next tile, finished CTAs}, 128 B apart).
-// Each launch takes the next slot round-robin; a slot returns to {0, 0} when the
-// launch using it finishes, so up to kSlots launches may be in flight at once.
+// Tile-scheduler slots ({next tile, finished CTAs}, 128 B apart), one per (device, stream).
+// Launches on one stream are ordered (every kernel starts with griddepcontrol.wait, and
+// the last CTA of a launch resets its slot to {0, 0} before the grid completes), so a slot
+// is never used by two grids at once as long as distinct streams get distinct slots. The
+// pool is allocated on first use per device, in relaxed capture mode so that a first call
+// made inside a CUDA-graph capture still works. Streams beyond kSchedSlots per device
+// share slots round-robin (not expected: one slot per concurrently used stream).
 constexpr int kSchedSlots = 256;
-inline unsigned int* sched_slot(int dev) {
+inline unsigned int* sched_slot(int dev, cudaStream_t s) {
+  struct Entry { int dev; cudaStream_t s; unsigned int slot; };
   static std::mutex mu;
   static unsigned int* pool[64] = {nullptr};
   static unsigned int next[64] = {0};
+  static std::vector<Entry> assigned;
   if (dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
   if (!pool[dev]) {
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
     void* p = nullptr;
-    if (cudaMalloc(&p, (size_t)kSchedSlots * 128) != cudaSuccess) {
+    bool ok = cudaMalloc(&p, (size_t)kSchedSlots * 128) == cudaSuccess;
+    if (ok) ok = cudaMemset(p, 0, (size_t)kSchedSlots * 128) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (!ok) {
       cudaGetLastError();
       return nullptr;
     }
-    cudaMemset(p, 0, (size_t)kSchedSlots * 128);
-    cudaDeviceSynchronize();
     pool[dev] = static_cast<unsigned int*>(p);
   }
+  for (const Entry& e : assigned)
+    if (e.dev == dev && e.s == s) return pool[dev] + e.slot * 32;
   const unsigned int slot = next[dev]++ % kSchedSlots;
+  assigned.push_back({dev, s, slot});
   return pool[dev] + slot * 32;
 }
 
@@ -197,7 +209,7 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   sms = sm_count(dev);
-  unsigned int* sched = sched_slot(dev);
+  unsigned int* sched = sched_slot(dev, s);
   if (!sched) return 0;
   tile::TileParams p;
   p.out = d_out;
@@ -263,7 +275,7 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   sms = sm_count(dev);
-  unsigned int* sched = sched_slot(dev);
+  unsigned int* sched = sched_slot(dev, s);
   if (!sched) return 0;
   tile::TileParams p;
   p.out = d_out;
@@ -390,7 +402,7 @@ inline int launch_warp_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   sms = sm_count(dev);
-  unsigned int* sched = sched_slot(dev);
+  unsigned int* sched = sched_slot(dev, s);
   if (!sched) return 0;
   tile::TileParams p;
   p.out = d_out;
@@ -483,20 +495,18 @@ inline int kernel_family() {
   return v;
 }
 
-template <int TH>
-inline int launch_k3_th(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int method,
-                        unsigned long long* counts, cudaStream_t s, bool* taken) {
-  using G = k3::Geo<TH>;
+template <int BAND, bool FULL, bool FNR>
+inline int launch_k3_kern(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int method,
+                          unsigned long long* counts, cudaStream_t s, bool* taken) {
+  using G = k3::Geo<BAND>;
   *taken = false;
   CUtensorMap in_map;
   const int out_rows = g.row_end - g.row_begin;
   if (!make_map<uint8_t>(&in_map, d_in, g.width, g.in_rows, g.batch, g.in_pitch, g.in_frame_stride, G::BOXW,
                          G::BOXH))
     return 0;
-  const bool full_w = g.width % k3::TW == 0;
-  static int bps[2] = {0, 0};
-  int& blocks_per_sm = bps[full_w ? 1 : 0];
-  auto kern = full_w ? k3::fnr_k3_kernel<TH, true> : k3::fnr_k3_kernel<TH, false>;
+  auto kern = k3::fnr_k3_kernel<BAND, FULL, FNR>;
+  static int blocks_per_sm = 0;
   if (blocks_per_sm == 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     int n = 0;
@@ -509,9 +519,9 @@ inline int launch_k3_th(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   sms = sm_count(dev);
-  unsigned int* sched = sched_slot(dev);
+  unsigned int* sched = sched_slot(dev, s);
   if (!sched) return 0;
-  tile::TileParams p;
+  tile::TileParams p = {};
   p.out = d_out;
   p.out_pitch = g.out_pitch;
   p.out_frame = g.out_frame_stride;
@@ -521,16 +531,12 @@ inline int launch_k3_th(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, 
   p.row_begin = g.row_begin;
   p.row_end = g.row_end;
   p.tiles_x = (g.width + k3::TW - 1) / k3::TW;
-  p.tiles_y = (out_rows + TH - 1) / TH;
+  p.tiles_y = (out_rows + G::TH - 1) / G::TH;
   p.batch = g.batch;
   p.method = method;
   p.counts = counts;
   p.sched = sched;
   p.one = 1u;
-  p.debug = 0;
-  p.full_tiles = 0;
-  p.static_rounds = 0;
-  p.debug_buf = nullptr;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));
@@ -544,17 +550,31 @@ inline int launch_k3_th(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, 
   return 0;
 }
 
-// Dense 3x3 kernel for u8 frames (fnr_k3.cuh): 128-row tiles, or 32-row tiles when the
-// job has fewer than two 128-row tiles per SM.
+template <int BAND>
+inline int launch_k3_band(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int method,
+                          unsigned long long* counts, cudaStream_t s, bool* taken) {
+  const bool full = g.width % k3::TW == 0 && (g.row_end - g.row_begin) % k3::Geo<BAND>::TH == 0;
+  if (full)
+    return method == 0 ? launch_k3_kern<BAND, true, true>(d_in, d_out, g, method, counts, s, taken)
+                       : launch_k3_kern<BAND, true, false>(d_in, d_out, g, method, counts, s, taken);
+  return method == 0 ? launch_k3_kern<BAND, false, true>(d_in, d_out, g, method, counts, s, taken)
+                     : launch_k3_kern<BAND, false, false>(d_in, d_out, g, method, counts, s, taken);
+}
+
+// Dense 3x3 kernel for u8 frames (fnr_k3.cuh). Tile height 160 / 128 / 64 / 32 rows: the
+// tallest one that divides the rows (whole tiles need no validity masks) while leaving at
+// least two tiles per SM; 32-row tiles for small jobs.
 inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int method,
                      unsigned long long* counts, cudaStream_t s, bool* taken) {
-  const long long tiles128 = (long long)((g.width + k3::TW - 1) / k3::TW) *
-                             ((g.row_end - g.row_begin + 127) / 128) * g.batch;
-  const long long tiles32 = (long long)((g.width + k3::TW - 1) / k3::TW) * ((g.row_end - g.row_begin + 31) / 32) *
-                            g.batch;
-  if (tiles32 < 148) return launch_k3_th<16>(d_in, d_out, g, method, counts, s, taken);  // c1: 128 tiles
-  if (tiles128 < 2 * 148) return launch_k3_th<32>(d_in, d_out, g, method, counts, s, taken);
-  return launch_k3_th<128>(d_in, d_out, g, method, counts, s, taken);
+  const long long rows = g.row_end - g.row_begin;
+  const long long tx = (g.width + k3::TW - 1) / k3::TW;
+  auto tiles = [&](int th) { return tx * ((rows + th - 1) / th) * g.batch; };
+  const long long enough = 2LL * 148;
+  if (rows % 160 == 0 && tiles(160) >= enough) return launch_k3_band<10>(d_in, d_out, g, method, counts, s, taken);
+  if (rows % 128 == 0 && tiles(128) >= enough) return launch_k3_band<8>(d_in, d_out, g, method, counts, s, taken);
+  if (rows % 64 == 0 && tiles(64) >= enough) return launch_k3_band<4>(d_in, d_out, g, method, counts, s, taken);
+  if (tiles(128) >= 4 * enough) return launch_k3_band<8>(d_in, d_out, g, method, counts, s, taken);
+  return launch_k3_band<2>(d_in, d_out, g, method, counts, s, taken);
 }
 
 template <typename T>

@@ -1,65 +1,149 @@
 // Dense 3x3 FNR / MF kernel for u8 frames (BASELINE configs c1, c5), sm_100a.
 //
-// For k = 3 the median network is cheap enough to evaluate for EVERY pixel, so
-// this kernel has no queue: detector, median and select all run branch-free on
-// packed words and the result goes straight to HBM.
+// For k = 3 the median is cheap enough to evaluate for EVERY pixel, so this kernel has
+// no queue: detector, median, select and counters run branch-free on packed words and
+// the result goes straight to HBM (reference filters.py:156-180).
 //
-// Packing: "vertical pair keys". A 32-bit word holds one column's pixels of two
-// consecutive rows, each as the 16-bit key v*257 (= byte v in both halves, built
-// by one PRMT from two row words). Keys are monotone in v and equality preserving,
-// so min/max/median on keys are min/max/median on pixels, and with two rows per
-// word the vertical neighbour comes from one PRMT and horizontal neighbours are
-// just other registers.
+// Keys. One 32-bit word holds one column's pixels of two consecutive rows, each as the
+// 16-bit key 0x6400 | v: as an unsigned integer it is monotone in v (so VIMNMX.U16x2
+// min / max / median on keys are min / max / median on pixels), and as an fp16 number it
+// is exactly 1024 + v (so differences of keys are exact small integers in f16x2
+// arithmetic). A word's lane 0 is the upper row. Keys are built from two row words with
+// two PRMTs per pair of columns plus one per column (interleave the rows, then insert
+// the 0x64 exponent byte).
 //
-// Per two output rows y, y+1 and column x (reference filters.py:156-180):
-//   column sort   lo/hi = min3/max3(A, S, B), mid = A+S+B-lo-hi   (A = rows y-1,y;
-//                 S = rows y,y+1; B = rows y+1,y+2: lanewise the 3-row window)
-//   median of 9   med3(max3(lo), med3(mid), min3(hi))  over columns x-1, x, x+1
-//                 (exact for 3x3: the classic sorted-columns identity)
-//   detector      c == min9 || c == max9, min9 = min3(lo), max9 = max3(hi)
-//   select        out = noisy ? median : c    (FNR)   /   out = median   (MF)
-// Sums a+b+c-min-max are exact in 32-bit arithmetic, so the IADDs run on the
-// FMA pipe while VIMNMX3 and PRMT use the ALU pipe.
+// Per step (two output rows y, y+1; A = keys of rows y-1,y; B = rows y+1,y+2;
+// S = rows y,y+1 = one PRMT of A and B), for each of COLS + 2 columns:
+//   column sort    lo = min3(A,S,B), hi = max3(A,S,B), mid = A+S+B-lo-hi   (lanewise the
+//                  sorted 3-row column of both output rows; the integer sum is exact in 32
+//                  bits because every lane of the result is in range)
+// and for each output column (columns j-1, j, j+1):
+//   median of 9    med3(max3(lo), med3(mid), min3(hi))  (the sorted-columns identity);
+//                  med3(mid) shares the sorted middle pair between horizontal neighbours:
+//                  p,q = sort(mid[j], mid[j+1]) serves outputs j-1 and j as clamp(., p, q)
+//   detector       min9 = min3(lo), max9 = max3(hi); noisy iff c == min9 or c == max9
+//   select (FNR)   in f16x2 on the FMA pipe: s = sat(1 + (min9 - c)(max9 - c)) is 1.0 for a
+//                  noisy lane and 0 otherwise; out = c + (med - c) s
+//   counters       detected += s, replaced += sat(|med - c| s), f16x2 accumulators
+//                  flushed to integers once per tile
+//   MF             out = med
+// The min/max network and the key shuffles issue on the ALU pipe, the f16x2 select and
+// counters and the sums on the FMA pipe (measured half-rate each, dual-issuing:
+// profiles/pipe_probe_r02.txt).
 #pragma once
+#include <cuda_fp16.h>
 #include "fnr_tile.cuh"
 
 namespace irdn {
 namespace k3 {
 
 constexpr int THREADS = 128;
-constexpr int TW = 128;                 // tile width (pixels)
-constexpr int COLS = 8;                 // columns per thread (one 8-byte row segment)
-constexpr int TPR = TW / COLS;          // threads per row band (16)
-constexpr int BANDS = THREADS / TPR;    // row bands per tile (8)
+constexpr int COLS = 16;                // output columns per thread (one 16-byte row segment)
+constexpr int TPR = 8;                  // threads per row band
+constexpr int TW = COLS * TPR;          // tile width: 128 pixels
+constexpr int BANDS = THREADS / TPR;    // 16 row bands per tile
 constexpr int NSTAGE = 2;
-// Tile height: 128 rows (16 per thread) for large frames, 32 rows (4 per thread) when a
-// frame has too few 128-row tiles to fill the GPU, 16 rows (2 per thread) when even
-// 32-row tiles leave SMs idle (BASELINE c1: 512x512 -> 128 tiles).
 
-template <int TH>
+// Pipe placement of the integer helper arithmetic (A/B switches; the defaults are the
+// measured best): the row-pair shift S and the column middle on the FMA pipe (IMADs), the
+// final median-of-3 sum on the ALU pipe (IADD3).
+#ifndef IRDN_K3_S_FMA
+#define IRDN_K3_S_FMA 0
+#endif
+#ifndef IRDN_K3_MID_FMA
+#define IRDN_K3_MID_FMA 1
+#endif
+#ifndef IRDN_K3_UNROLL
+#define IRDN_K3_UNROLL 1
+#endif
+#ifndef IRDN_K3_FIN_FMA
+#define IRDN_K3_FIN_FMA 0
+#endif
+constexpr int kStepUnroll = IRDN_K3_UNROLL;
+
+// Tile height TH = BANDS * BAND (BAND = rows per thread, even): 160 (BAND 10), 128, 64 or 32.
+template <int BAND>
 struct Geo {
-  static constexpr int r = 1;
-  static constexpr int A = 16;  // TMA box x start must be 16-byte aligned
-  static constexpr int R = A;
-  static constexpr int BOXW = ((TW + R + r + A - 1) / A) * A;  // 160
-  static constexpr int BOXH = TH + 2 * r;                      // 130
+  static_assert(BAND % 2 == 0, "two output rows per step");
+  static constexpr int TH = BANDS * BAND;
+  static constexpr int R = 16;          // left halo: TMA box x start must be 16-byte aligned
+  static constexpr int BOXW = TW + 2 * R;  // 160: tile columns -16 .. 143
+  static constexpr int BOXH = TH + 2;
   static constexpr int IN_BYTES = BOXW * BOXH;
   static constexpr int IN_STRIDE = (IN_BYTES + 127) & ~127;
   static constexpr int BAR_OFF = NSTAGE * IN_STRIDE;
   static constexpr int TILE_OFF = BAR_OFF + 8 * NSTAGE;
   static constexpr int SMEM = TILE_OFF + 16 * NSTAGE + 128;
+  static_assert(BOXH <= 256, "TMA box limit");
 };
 
-// Median of three packed keys: a + b + c - min - max (exact in 32-bit: the true median
-// fits each lane). The 3-input sum stays one IADD3; the subtraction goes to the FMA pipe.
-__device__ __forceinline__ uint32_t med3(uint32_t a, uint32_t b, uint32_t c, uint32_t m1) {
-  return fma_sub(fma_sub(a + b + c, m1, vmin3(a, b, c)), m1, vmax3(a, b, c));
+// ---- f16x2 helpers (FMA pipe) ----------------------------------------------------
+__device__ __forceinline__ uint32_t hsub(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t hadd(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t hfma(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ uint32_t hfma_sat(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("fma.rn.sat.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+// sat(|a| * b)
+__device__ __forceinline__ uint32_t hmul_sat_abs(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("{.reg .b32 t; abs.f16x2 t, %1; mul.rn.sat.f16x2 %0, t, %2;}" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+// Both f16 lanes of an accumulator as one integer (each lane holds an exact count <= 2048).
+__device__ __forceinline__ uint32_t hsum_lanes(uint32_t h) {
+  const __half2 v = *reinterpret_cast<const __half2*>(&h);
+  return (uint32_t)(__half2float(__low2half(v)) + __half2float(__high2half(v)));
 }
 
-// Replicate-edge fix-up (see tile::fix_edges) for this kernel's box.
-template <int TH>
+constexpr uint32_t KEY_BYTE = 0x64646464u;  // f16 exponent byte of 1024 + v
+constexpr uint32_t F16_ONE = 0x3C003C00u;
+
+// A row segment of one thread: 16 pixels at tile columns x0 .. x0+15 plus the words
+// holding columns x0-1 (byte 3 of `l`) and x0+16 (byte 0 of `r`).
+struct RowSeg {
+  uint4 m;
+  uint32_t l, r;
+};
+__device__ __forceinline__ void load_seg(const uint8_t* p, RowSeg& s) {
+  s.m = *reinterpret_cast<const uint4*>(p);
+  s.l = *reinterpret_cast<const uint32_t*>(p - 4);
+  s.r = *reinterpret_cast<const uint32_t*>(p + 16);
+}
+// Keys of columns x0-1 .. x0+16 (k[0] .. k[COLS+1]) for rows (t, b): lane 0 = row t.
+__device__ __forceinline__ void make_keys(const RowSeg& t, const RowSeg& b, uint32_t (&k)[COLS + 2]) {
+  k[0] = tile::prmt(tile::prmt(t.l, b.l, 0x7733u), KEY_BYTE, 0x4240u);  // (t3, t3, b3, b3) -> (t3, 64, b3, 64)
+  const uint32_t tw[4] = {t.m.x, t.m.y, t.m.z, t.m.w}, bw[4] = {b.m.x, b.m.y, b.m.z, b.m.w};
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t i0 = tile::prmt(tw[w], bw[w], 0x5140u);  // (t0, b0, t1, b1)
+    const uint32_t i1 = tile::prmt(tw[w], bw[w], 0x7362u);  // (t2, b2, t3, b3)
+    k[1 + 4 * w] = tile::prmt(i0, KEY_BYTE, 0x4140u);
+    k[2 + 4 * w] = tile::prmt(i0, KEY_BYTE, 0x4342u);
+    k[3 + 4 * w] = tile::prmt(i1, KEY_BYTE, 0x4140u);
+    k[4 + 4 * w] = tile::prmt(i1, KEY_BYTE, 0x4342u);
+  }
+  k[COLS + 1] = tile::prmt(tile::prmt(t.r, b.r, 0x4400u), KEY_BYTE, 0x4240u);
+}
+
+// Replicate-edge fix-up of the box cells outside the frame (see tile::fix_edges).
+template <int BAND>
 __device__ __forceinline__ void fix_edges(uint8_t* s_in, int gx_lo, int gy_lo, int width, int height) {
-  constexpr int BOXW = Geo<TH>::BOXW, BOXH = Geo<TH>::BOXH, A = Geo<TH>::A;
+  constexpr int BOXW = Geo<BAND>::BOXW, BOXH = Geo<BAND>::BOXH, A = Geo<BAND>::R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c_lo = max(0, -gx_lo), c_hi = min(BOXW, width - gx_lo);
   const int y_lo = max(0, -gy_lo), y_hi = min(BOXH, height - gy_lo);
@@ -96,31 +180,12 @@ __device__ __forceinline__ void fix_edges(uint8_t* s_in, int gx_lo, int gy_lo, i
   }
 }
 
-// Keys of the 10 columns x-1 .. x+8 for smem rows `ra` and `ra + 1` (lane 0 = row ra).
-template <int BOXW>
-__device__ __forceinline__ void load_keys(const uint8_t* s_row, uint32_t (&key)[COLS + 2]) {
-  const uint8_t* p1 = s_row;
-  const uint8_t* p2 = s_row + BOXW;
-  const uint32_t l1 = *reinterpret_cast<const uint32_t*>(p1 - 4), l2 = *reinterpret_cast<const uint32_t*>(p2 - 4);
-  const uint2 m1 = *reinterpret_cast<const uint2*>(p1), m2 = *reinterpret_cast<const uint2*>(p2);
-  const uint32_t r1 = *reinterpret_cast<const uint32_t*>(p1 + 8), r2 = *reinterpret_cast<const uint32_t*>(p2 + 8);
-  key[0] = tile::prmt(l1, l2, 0x7733u);  // column x-1 = byte 3 of the left word
-  key[1] = tile::prmt(m1.x, m2.x, 0x4400u);
-  key[2] = tile::prmt(m1.x, m2.x, 0x5511u);
-  key[3] = tile::prmt(m1.x, m2.x, 0x6622u);
-  key[4] = tile::prmt(m1.x, m2.x, 0x7733u);
-  key[5] = tile::prmt(m1.y, m2.y, 0x4400u);
-  key[6] = tile::prmt(m1.y, m2.y, 0x5511u);
-  key[7] = tile::prmt(m1.y, m2.y, 0x6622u);
-  key[8] = tile::prmt(m1.y, m2.y, 0x7733u);
-  key[9] = tile::prmt(r1, r2, 0x4400u);  // column x+8 = byte 0 of the right word
-}
-
-template <int TH, bool FULL_W>
+// FULL: every tile of the launch is whole (width % TW == 0, rows % TH == 0), so no
+// row / column validity masks are evaluated. FNR: method "fnr" (else "mf").
+template <int BAND, bool FULL, bool FNR>
 __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__ CUtensorMap in_map,
                                                          const tile::TileParams p) {
-  using G = Geo<TH>;
-  constexpr int BAND = TH / BANDS;  // rows per thread
+  using G = Geo<BAND>;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((128u - (tile::smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + G::BAR_OFF);
@@ -130,9 +195,8 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
   const int tid = threadIdx.x;
   const int tiles_per_frame = p.tiles_x * p.tiles_y;
   const int ntiles = tiles_per_frame * p.batch;
-  const bool fnr = p.method == 0;
-  const uint32_t one = p.one, m1 = 0u - p.one, k65536 = p.one << 16;  // opaque constants for the FMA pipe
   uint32_t det_total = 0, rep_total = 0;
+  const uint32_t one = p.one, m1 = 0u - p.one, k65536 = p.one << 16;  // opaque: keeps IMADs on the FMA pipe
 
   auto refill = [&](int stage) {
     tile::TileInfo ti;
@@ -142,11 +206,11 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
       const int tt = ti.t - ti.b * tiles_per_frame;
       const int ty = tt / p.tiles_x;
       ti.tx0 = (tt - ty * p.tiles_x) * TW;
-      ti.ty0 = p.row_begin + ty * TH;
+      ti.ty0 = p.row_begin + ty * G::TH;
       s_tile[stage] = ti;
       tile::mbar_expect_tx(&s_bar[stage], G::IN_BYTES);
-      tile::tma_load_3d(smem + stage * G::IN_STRIDE, &in_map, &s_bar[stage], ti.tx0 - G::R, ti.ty0 - 1 - p.in_row0,
-                        ti.b);
+      tile::tma_load_3d(smem + stage * G::IN_STRIDE, &in_map, &s_bar[stage], ti.tx0 - G::R,
+                        ti.ty0 - 1 - p.in_row0, ti.b);
     } else {
       s_tile[stage] = ti;
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tile::smem_u32(&s_bar[stage])) : "memory");
@@ -162,8 +226,8 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
   __syncthreads();
 
   const int tc = tid % TPR, band = tid / TPR;
-  const int x0 = tc * COLS;       // first tile column of this thread
-  const int y0 = band * BAND;     // first tile row of this thread
+  const int x0 = tc * COLS;   // first tile column of this thread
+  const int y0 = band * BAND;  // first tile row of this thread
   uint8_t* const out_base = reinterpret_cast<uint8_t*>(p.out);
 
   for (int iter = 0;; ++iter) {
@@ -174,86 +238,124 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
     if (ti.t >= ntiles) break;
     const int gx_lo = ti.tx0 - G::R, gy_lo = ti.ty0 - 1;
     if (gx_lo < 0 || gy_lo < 0 || gx_lo + G::BOXW > p.width || gy_lo + G::BOXH > p.height) {
-      fix_edges<TH>(smem + stage * G::IN_STRIDE, gx_lo, gy_lo, p.width, p.height);
+      fix_edges<BAND>(smem + stage * G::IN_STRIDE, gx_lo, gy_lo, p.width, p.height);
       __syncthreads();
     }
-    const int valid_w = min(TW, p.width - ti.tx0);
-    const int valid_h = min(TH, p.row_end - ti.ty0);
+    int valid_w = TW, valid_h = G::TH;
+    if constexpr (!FULL) {
+      valid_w = min(TW, p.width - ti.tx0);
+      valid_h = min(G::TH, p.row_end - ti.ty0);
+    }
     uint8_t* outp = out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.ty0 - p.row_begin + y0) * p.out_pitch +
                     ti.tx0 + x0;
-    // column validity (only when the frame width is not a multiple of the tile)
-    uint32_t colkeep[COLS];
-#pragma unroll
-    for (int i = 0; i < COLS; ++i) colkeep[i] = (FULL_W || x0 + i < valid_w) ? 0u : 0xFFFFFFFFu;
-
-    // smem row of output row y is y + 1; the first pair A covers smem rows y0, y0+1
-    const uint8_t* srow = s_in + y0 * G::BOXW + x0 + G::R;
+    // smem row of tile row y is y + 1; the thread's segment starts at box column R + x0
+    const uint8_t* srow = s_in + y0 * G::BOXW + G::R + x0;
     uint32_t A[COLS + 2];
-    load_keys<G::BOXW>(srow, A);
-    uint32_t keep_acc = 0, rep_acc = 0;
-#pragma unroll (BAND >= 8 ? 2 : 1)
+    {
+      RowSeg r0, r1;
+      load_seg(srow, r0);
+      load_seg(srow + G::BOXW, r1);
+      make_keys(r0, r1, A);
+    }
+    uint32_t dacc = 0, racc = 0;  // f16x2 counters of this tile
+#pragma unroll (kStepUnroll)
     for (int s = 0; s < BAND / 2; ++s) {
       uint32_t B[COLS + 2];
-      load_keys<G::BOXW>(srow + (2 * s + 2) * G::BOXW, B);
+      {
+        RowSeg r1, r2;
+        load_seg(srow + (2 * s + 2) * G::BOXW, r1);
+        load_seg(srow + (2 * s + 3) * G::BOXW, r2);
+        make_keys(r1, r2, B);
+      }
       uint32_t lo[COLS + 2], hi[COLS + 2], mid[COLS + 2], S[COLS + 2];
 #pragma unroll
       for (int c = 0; c < COLS + 2; ++c) {
-        S[c] = shift_pair(A[c], B[c], k65536);  // rows y, y+1
+        if (IRDN_K3_S_FMA == 1 || (IRDN_K3_S_FMA == 2 && (c & 1)))
+          S[c] = shift_pair(A[c], B[c], k65536);  // rows y, y+1 (IMAD.HI + IMAD)
+        else
+          S[c] = tile::prmt(A[c], B[c], 0x5432u);  // rows y, y+1
         lo[c] = vmin3(A[c], S[c], B[c]);
         hi[c] = vmax3(A[c], S[c], B[c]);
-        mid[c] = fma_sub(fma_sub(A[c] + S[c] + B[c], m1, lo[c]), m1, hi[c]);
+#if IRDN_K3_MID_FMA
+        mid[c] = fma_sub(fma_sub(fma_add(B[c], one, fma_add(A[c], one, S[c])), m1, lo[c]), m1, hi[c]);
+#else
+        mid[c] = A[c] + S[c] + B[c] - lo[c] - hi[c];
+#endif
         A[c] = B[c];
       }
-      const int yr = y0 + 2 * s;  // tile row of lane 0
-      const uint32_t rowkeep = (yr < valid_h ? 0u : 0x0000FFFFu) | (yr + 1 < valid_h ? 0u : 0xFFFF0000u);
+      uint32_t rowmask = 0xFFFFFFFFu;  // non-FULL: lanes of rows inside the tile
+      if constexpr (!FULL) {
+        const int yr = y0 + 2 * s;
+        rowmask = (yr < valid_h ? 0x0000FFFFu : 0u) | (yr + 1 < valid_h ? 0xFFFF0000u : 0u);
+      }
       uint32_t out[COLS];
 #pragma unroll
-      for (int i = 0; i < COLS; ++i) {
-        const uint32_t med = med3(vmax3(lo[i], lo[i + 1], lo[i + 2]), med3(mid[i], mid[i + 1], mid[i + 2], m1),
-                                  vmin3(hi[i], hi[i + 1], hi[i + 2]), m1);
-        if (fnr) {
-          const uint32_t c = S[i + 1];
-          const uint32_t mn = vmin3(lo[i], lo[i + 1], lo[i + 2]), mx = vmax3(hi[i], hi[i + 1], hi[i + 2]);
-          // lane of m == 0 <=> centre is the window min or max; m <= 0x7FFF so +0x7FFF sets bit 15 iff m != 0
-          const uint32_t e = fma_add(vmin2(fma_sub(c, m1, mn), fma_sub(mx, m1, c)), one, 0x7FFF7FFFu);
-          uint32_t keep = tile::prmt(e, e, 0xBB99u);  // 0xFFFF lanes: signal pixel, keep the centre
-          keep |= rowkeep | colkeep[i];
-          out[i] = (c & keep) | (med & ~keep);
-          keep_acc = fma_add(keep, one, keep_acc);                          // decoded per tile (see below)
-          rep_acc = fma_add(vmin2((med ^ c) & ~keep, 0x00010001u), one, rep_acc);  // noisy and changed
-        } else {
-          out[i] = med;
+      for (int j = 0; j < COLS; j += 2) {
+        const uint32_t pm = vmin2(mid[j + 1], mid[j + 2]), qm = vmax2(mid[j + 1], mid[j + 2]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int o = j + h;  // output column o: key columns o, o+1, o+2
+          const uint32_t md = vmax2(pm, vmin2(qm, mid[h == 0 ? j : j + 3]));
+          const uint32_t mxlo = vmax3(lo[o], lo[o + 1], lo[o + 2]);
+          const uint32_t mnhi = vmin3(hi[o], hi[o + 1], hi[o + 2]);
+          const uint32_t mn3 = vmin3(mxlo, md, mnhi), mx3 = vmax3(mxlo, md, mnhi);
+          uint32_t med;
+          if (IRDN_K3_FIN_FMA == 1 || (IRDN_K3_FIN_FMA == 2 && h == 1))
+            med = fma_sub(fma_sub(fma_add(mnhi, one, fma_add(mxlo, one, md)), m1, mn3), m1, mx3);
+          else
+            med = mxlo + md + mnhi - mn3 - mx3;
+          if constexpr (FNR) {
+            const uint32_t c = S[o + 1];
+            const uint32_t mn = vmin3(lo[o], lo[o + 1], lo[o + 2]), mx = vmax3(hi[o], hi[o + 1], hi[o + 2]);
+            uint32_t sflag = hfma_sat(hsub(mn, c), hsub(mx, c), F16_ONE);  // 1.0: noisy lane
+            const uint32_t dm = hsub(med, c);
+            out[o] = hfma(dm, sflag, c);
+            if constexpr (!FULL) {
+              const bool colok = x0 + o < valid_w;
+              sflag &= colok ? rowmask : 0u;
+            }
+            racc = hadd(racc, hmul_sat_abs(dm, sflag));
+            dacc = hadd(dacc, sflag);
+          } else {
+            out[o] = med;
+          }
         }
       }
-      // keys -> bytes: both halves of a key hold the pixel value
-      const uint32_t q01 = tile::prmt(out[0], out[1], 0x6240u), q23 = tile::prmt(out[2], out[3], 0x6240u);
-      const uint32_t q45 = tile::prmt(out[4], out[5], 0x6240u), q67 = tile::prmt(out[6], out[7], 0x6240u);
-      const uint2 row_a = make_uint2(tile::prmt(q01, q23, 0x5410u), tile::prmt(q45, q67, 0x5410u));
-      const uint2 row_b = make_uint2(tile::prmt(q01, q23, 0x7632u), tile::prmt(q45, q67, 0x7632u));
-      if (FULL_W) {
-        if (yr < valid_h) *reinterpret_cast<uint2*>(outp) = row_a;
-        if (yr + 1 < valid_h) *reinterpret_cast<uint2*>(outp + p.out_pitch) = row_b;
-      } else {
-        const uint8_t* ba = reinterpret_cast<const uint8_t*>(&row_a);
-        const uint8_t* bb = reinterpret_cast<const uint8_t*>(&row_b);
+      // keys -> bytes: byte 0 of a key is the upper row's pixel, byte 2 the lower row's
+      uint32_t row_a[COLS / 4], row_b[COLS / 4];
 #pragma unroll
-        for (int i = 0; i < COLS; ++i) {
-          if (x0 + i < valid_w) {
-            if (yr < valid_h) outp[i] = ba[i];
-            if (yr + 1 < valid_h) outp[p.out_pitch + i] = bb[i];
+      for (int w = 0; w < COLS / 4; ++w) {
+        const uint32_t q01 = tile::prmt(out[4 * w], out[4 * w + 1], 0x6240u);
+        const uint32_t q23 = tile::prmt(out[4 * w + 2], out[4 * w + 3], 0x6240u);
+        row_a[w] = tile::prmt(q01, q23, 0x5410u);
+        row_b[w] = tile::prmt(q01, q23, 0x7632u);
+      }
+      if constexpr (FULL) {
+        *reinterpret_cast<uint4*>(outp) = make_uint4(row_a[0], row_a[1], row_a[2], row_a[3]);
+        *reinterpret_cast<uint4*>(outp + p.out_pitch) = make_uint4(row_b[0], row_b[1], row_b[2], row_b[3]);
+      } else {
+        const int yr = y0 + 2 * s;
+        const uint8_t* ba = reinterpret_cast<const uint8_t*>(row_a);
+        const uint8_t* bb = reinterpret_cast<const uint8_t*>(row_b);
+        if (x0 + COLS <= valid_w) {
+          if (yr < valid_h) *reinterpret_cast<uint4*>(outp) = make_uint4(row_a[0], row_a[1], row_a[2], row_a[3]);
+          if (yr + 1 < valid_h)
+            *reinterpret_cast<uint4*>(outp + p.out_pitch) = make_uint4(row_b[0], row_b[1], row_b[2], row_b[3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < COLS; ++i) {
+            if (x0 + i < valid_w) {
+              if (yr < valid_h) outp[i] = ba[i];
+              if (yr + 1 < valid_h) outp[p.out_pitch + i] = bb[i];
+            }
           }
         }
       }
       outp += 2 * p.out_pitch;
     }
-    if (fnr) {
-      // keep_acc = sum of lane masks 0xFFFF: as integers it is 65535*K0 - 65536*K1 (mod 2^32)
-      // for K0 / K1 kept lane-0 / lane-1 pixels, K0, K1 <= BAND/2*COLS
-      const uint32_t k0 = (0u - keep_acc) & 0xFFFFu;
-      const int diff = (int)(int16_t)(uint16_t)((keep_acc + k0) >> 16);  // K0 - K1
-      const uint32_t kept = 2u * k0 - (uint32_t)diff;
-      det_total += (uint32_t)(BAND * COLS) - kept;
-      rep_total += (rep_acc & 0xFFFFu) + (rep_acc >> 16);
+    if constexpr (FNR) {
+      det_total += hsum_lanes(dacc);
+      rep_total += hsum_lanes(racc);
     }
     tile::fence_proxy_async();
     __syncthreads();
@@ -263,7 +365,7 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
     p.sched[0] = 0u;
     p.sched[1] = 0u;
   }
-  if (fnr) block_add_counts<THREADS>(det_total, rep_total, p.counts);
+  if constexpr (FNR) block_add_counts<THREADS>(det_total, rep_total, p.counts);
 }
 
 }  // namespace k3

@@ -107,15 +107,18 @@ CONFIGS: dict[str, SceneConfig] = {
 
 
 def generate(cfg: SceneConfig, frame0: int = 0, nframes: int | None = None, seed: int = SEED,
-             threads: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
-    """Frames [frame0, frame0+nframes) of `cfg` as a [B,H,W] array (or into `out`)."""
+             threads: int | None = None, out: np.ndarray | None = None, lib=None) -> np.ndarray:
+    """Frames [frame0, frame0+nframes) of `cfg` as a [B,H,W] array (or into `out`).
+
+    `lib` is any loaded library exporting scene_generate (default: libirdn_scene.so; the
+    reference arm of bench.py passes its CPU checker library, which links the same source)."""
     n = cfg.frames if nframes is None else nframes
     if out is None:
         out = np.empty((n, cfg.height, cfg.width), dtype=cfg.np_dtype)
     assert out.flags.c_contiguous and out.dtype == cfg.np_dtype and out.size == n * cfg.height * cfg.width
     p = cfg.params(seed)
     nt = threads or max(1, min(32, os.cpu_count() or 1))
-    rc = load_scene_lib().scene_generate(ctypes.byref(p), frame0, n, out.ctypes.data, nt)
+    rc = (lib or load_scene_lib()).scene_generate(ctypes.byref(p), frame0, n, out.ctypes.data, nt)
     if rc != 0:
         raise ValueError("scene_generate rejected the parameters")
     return out

@@ -32,13 +32,50 @@ def test_reference_arm_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["workload"].startswith("c1")
+    # the reference arm's config block is the B200 arm's (the driver compares them)
+    import bench
+    from paper_1201_3972_b200.scene import CONFIGS
+
+    assert d["config"] == bench.config_block(CONFIGS["c1"], 1, 1)
+
+
+def test_default_workload_is_the_largest_single_gpu_config():
+    import bench
+    from paper_1201_3972_b200.scene import CONFIGS
+
+    sys.argv = ["bench.py"]
+    assert bench.parse().config == "c5"
+    assert max(CONFIGS.values(), key=lambda c: c.pixels).name == "c5"
+
+
+def test_work_split_follows_the_survey_plan():
+    """c2/c3/c5 split frames, c4 row strips with r-row halos, c1 replicas."""
+    import bench
+    from paper_1201_3972_b200.scene import CONFIGS
+
+    for name in ("c2", "c3", "c5"):
+        cfg = CONFIGS[name]
+        for n in (1, 2, 4, 8):
+            shares = [bench.rank_share(cfg, n, r) for r in range(n)]
+            assert [s["f0"] for s in shares] == [cfg.frames * r // n for r in range(n)]
+            assert sum(s["f1"] - s["f0"] for s in shares) == cfg.frames
+    c4 = CONFIGS["c4"]
+    for n in (2, 4, 8):
+        shares = [bench.rank_share(c4, n, r) for r in range(n)]
+        assert shares[0]["in0"] == 0 and shares[-1]["in1"] == c4.height
+        assert sum(s["y1"] - s["y0"] for s in shares) == c4.height
+        for s in shares:
+            assert s["kind"] == "rows" and s["y0"] - s["in0"] <= 5 and s["in1"] - s["y1"] <= 5
+    assert bench.rank_share(CONFIGS["c1"], 4, 3)["replica"]
+    assert bench.scaling_kind(CONFIGS["c1"], 4) == "weak" and bench.scaling_kind(c4, 4) == "strong"
 
 
 @pytest.mark.gpu
 def test_b200_arm_line(cuda_ok):
     d = _run(["--steps", "50", "--warmup", "3", "--cpu-seconds", "1"])
     assert BASE_KEYS <= set(d) and "impl" not in d
-    assert d["config"]["workload"].startswith("c2") and d["dtype"] == "u16"
+    assert d["config"]["workload"].startswith("c5") and d["dtype"] == "u8"
+    assert d["roofline"]["static_ops"]["minmax_instr_per_px"] > 0
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
@@ -50,7 +87,7 @@ def test_b200_arm_line(cuda_ok):
 
 @pytest.mark.gpu
 def test_b200_arm_passes2_and_widened_rows(cuda_ok):
-    d = _run(["--steps", "20", "--warmup", "3", "--passes", "2", "--no-cpu-baseline"])
+    d = _run(["--config", "c2", "--steps", "20", "--warmup", "3", "--passes", "2", "--no-cpu-baseline"])
     assert d["config"]["passes"] == 2 and d["gpu_launches"] >= 40
     for path in ("noise", "sqerr"):
         d = _run(["--path", path, "--steps", "10", "--warmup", "3", "--cpu-seconds", "1"])
