@@ -561,17 +561,22 @@ inline int launch_k3_band(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g
                      : launch_k3_kern<BAND, false, false>(d_in, d_out, g, method, counts, s, taken);
 }
 
-// Dense 3x3 kernel for u8 frames (fnr_k3.cuh). Tile height 160 / 128 / 64 / 32 rows: the
-// tallest one that divides the rows (whole tiles need no validity masks) while leaving at
-// least two tiles per SM; 32-row tiles for small jobs.
+// Dense 3x3 kernel for u8 frames (fnr_k3.cuh). Tile height 160 / 128 / 96 / 64 / 32 rows:
+// the tallest one that divides the rows (then no tile needs validity masks) while leaving
+// at least two tiles per SM; else 128-row tiles (masked last row of tiles) for large jobs
+// and 32-row tiles for small ones (BASELINE c1: 64 tiles of 128 x 32).
 inline int launch_k3(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g, int method,
                      unsigned long long* counts, cudaStream_t s, bool* taken) {
   const long long rows = g.row_end - g.row_begin;
   const long long tx = (g.width + k3::TW - 1) / k3::TW;
   auto tiles = [&](int th) { return tx * ((rows + th - 1) / th) * g.batch; };
   const long long enough = 2LL * 148;
+#ifdef IRDN_K3_BAND
+  return launch_k3_band<IRDN_K3_BAND>(d_in, d_out, g, method, counts, s, taken);
+#endif
   if (rows % 160 == 0 && tiles(160) >= enough) return launch_k3_band<10>(d_in, d_out, g, method, counts, s, taken);
   if (rows % 128 == 0 && tiles(128) >= enough) return launch_k3_band<8>(d_in, d_out, g, method, counts, s, taken);
+  if (rows % 96 == 0 && tiles(96) >= enough) return launch_k3_band<6>(d_in, d_out, g, method, counts, s, taken);
   if (rows % 64 == 0 && tiles(64) >= enough) return launch_k3_band<4>(d_in, d_out, g, method, counts, s, taken);
   if (tiles(128) >= 4 * enough) return launch_k3_band<8>(d_in, d_out, g, method, counts, s, taken);
   return launch_k3_band<2>(d_in, d_out, g, method, counts, s, taken);

@@ -32,6 +32,7 @@
 // profiles/pipe_probe_r02.txt).
 #pragma once
 #include <cuda_fp16.h>
+#include <type_traits>
 #include "fnr_tile.cuh"
 
 namespace irdn {
@@ -42,7 +43,10 @@ constexpr int COLS = 16;                // output columns per thread (one 16-byt
 constexpr int TPR = 8;                  // threads per row band
 constexpr int TW = COLS * TPR;          // tile width: 128 pixels
 constexpr int BANDS = THREADS / TPR;    // 16 row bands per tile
-constexpr int NSTAGE = 2;
+#ifndef IRDN_K3_NSTAGE
+#define IRDN_K3_NSTAGE 1  // measured: 1 stage x 8 CTAs/SM beats 2 stages x 4 (c5 0.789 vs 0.797 ms)
+#endif
+constexpr int NSTAGE = IRDN_K3_NSTAGE;
 
 // Pipe placement of the integer helper arithmetic (A/B switches; the defaults are the
 // measured best): the row-pair shift S and the column middle on the FMA pipe (IMADs), the
@@ -180,8 +184,9 @@ __device__ __forceinline__ void fix_edges(uint8_t* s_in, int gx_lo, int gy_lo, i
   }
 }
 
-// FULL: every tile of the launch is whole (width % TW == 0, rows % TH == 0), so no
-// row / column validity masks are evaluated. FNR: method "fnr" (else "mf").
+// FULL: every tile of the launch is whole (width % TW == 0, rows % TH == 0): one unmasked
+// tile body. Otherwise the whole tiles still take the unmasked body and only the last
+// column / row of tiles the masked one (a CTA-uniform branch). FNR: method "fnr" (else "mf").
 template <int BAND, bool FULL, bool FNR>
 __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__ CUtensorMap in_map,
                                                          const tile::TileParams p) {
@@ -241,118 +246,123 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
       fix_edges<BAND>(smem + stage * G::IN_STRIDE, gx_lo, gy_lo, p.width, p.height);
       __syncthreads();
     }
-    int valid_w = TW, valid_h = G::TH;
-    if constexpr (!FULL) {
-      valid_w = min(TW, p.width - ti.tx0);
-      valid_h = min(G::TH, p.row_end - ti.ty0);
-    }
-    uint8_t* outp = out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.ty0 - p.row_begin + y0) * p.out_pitch +
-                    ti.tx0 + x0;
-    // smem row of tile row y is y + 1; the thread's segment starts at box column R + x0
-    const uint8_t* srow = s_in + y0 * G::BOXW + G::R + x0;
-    uint32_t A[COLS + 2];
-    {
-      RowSeg r0, r1;
-      load_seg(srow, r0);
-      load_seg(srow + G::BOXW, r1);
-      make_keys(r0, r1, A);
-    }
     uint32_t dacc = 0, racc = 0;  // f16x2 counters of this tile
-#pragma unroll (kStepUnroll)
-    for (int s = 0; s < BAND / 2; ++s) {
-      uint32_t B[COLS + 2];
+    auto body = [&](auto masked) {
+      constexpr bool MASKED = decltype(masked)::value;
+      int valid_w = TW, valid_h = G::TH;
+      if constexpr (MASKED) {
+        valid_w = min(TW, p.width - ti.tx0);
+        valid_h = min(G::TH, p.row_end - ti.ty0);
+      }
+      uint8_t* outp = out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.ty0 - p.row_begin + y0) * p.out_pitch +
+                      ti.tx0 + x0;
+      // smem row of tile row y is y + 1; the thread's segment starts at box column R + x0
+      const uint8_t* srow = s_in + y0 * G::BOXW + G::R + x0;
+      uint32_t A[COLS + 2];
       {
-        RowSeg r1, r2;
-        load_seg(srow + (2 * s + 2) * G::BOXW, r1);
-        load_seg(srow + (2 * s + 3) * G::BOXW, r2);
-        make_keys(r1, r2, B);
+        RowSeg r0, r1;
+        load_seg(srow, r0);
+        load_seg(srow + G::BOXW, r1);
+        make_keys(r0, r1, A);
       }
-      uint32_t lo[COLS + 2], hi[COLS + 2], mid[COLS + 2], S[COLS + 2];
-#pragma unroll
-      for (int c = 0; c < COLS + 2; ++c) {
-        if (IRDN_K3_S_FMA == 1 || (IRDN_K3_S_FMA == 2 && (c & 1)))
-          S[c] = shift_pair(A[c], B[c], k65536);  // rows y, y+1 (IMAD.HI + IMAD)
-        else
-          S[c] = tile::prmt(A[c], B[c], 0x5432u);  // rows y, y+1
-        lo[c] = vmin3(A[c], S[c], B[c]);
-        hi[c] = vmax3(A[c], S[c], B[c]);
-#if IRDN_K3_MID_FMA
-        mid[c] = fma_sub(fma_sub(fma_add(B[c], one, fma_add(A[c], one, S[c])), m1, lo[c]), m1, hi[c]);
-#else
-        mid[c] = A[c] + S[c] + B[c] - lo[c] - hi[c];
-#endif
-        A[c] = B[c];
-      }
-      uint32_t rowmask = 0xFFFFFFFFu;  // non-FULL: lanes of rows inside the tile
-      if constexpr (!FULL) {
-        const int yr = y0 + 2 * s;
-        rowmask = (yr < valid_h ? 0x0000FFFFu : 0u) | (yr + 1 < valid_h ? 0xFFFF0000u : 0u);
-      }
-      uint32_t out[COLS];
-#pragma unroll
-      for (int j = 0; j < COLS; j += 2) {
-        const uint32_t pm = vmin2(mid[j + 1], mid[j + 2]), qm = vmax2(mid[j + 1], mid[j + 2]);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int o = j + h;  // output column o: key columns o, o+1, o+2
-          const uint32_t md = vmax2(pm, vmin2(qm, mid[h == 0 ? j : j + 3]));
-          const uint32_t mxlo = vmax3(lo[o], lo[o + 1], lo[o + 2]);
-          const uint32_t mnhi = vmin3(hi[o], hi[o + 1], hi[o + 2]);
-          const uint32_t mn3 = vmin3(mxlo, md, mnhi), mx3 = vmax3(mxlo, md, mnhi);
-          uint32_t med;
-          if (IRDN_K3_FIN_FMA == 1 || (IRDN_K3_FIN_FMA == 2 && h == 1))
-            med = fma_sub(fma_sub(fma_add(mnhi, one, fma_add(mxlo, one, md)), m1, mn3), m1, mx3);
+  #pragma unroll (kStepUnroll)
+      for (int s = 0; s < BAND / 2; ++s) {
+        uint32_t B[COLS + 2];
+        {
+          RowSeg r1, r2;
+          load_seg(srow + (2 * s + 2) * G::BOXW, r1);
+          load_seg(srow + (2 * s + 3) * G::BOXW, r2);
+          make_keys(r1, r2, B);
+        }
+        uint32_t lo[COLS + 2], hi[COLS + 2], mid[COLS + 2], S[COLS + 2];
+  #pragma unroll
+        for (int c = 0; c < COLS + 2; ++c) {
+          if (IRDN_K3_S_FMA == 1 || (IRDN_K3_S_FMA == 2 && (c & 1)))
+            S[c] = shift_pair(A[c], B[c], k65536);  // rows y, y+1 (IMAD.HI + IMAD)
           else
-            med = mxlo + md + mnhi - mn3 - mx3;
-          if constexpr (FNR) {
-            const uint32_t c = S[o + 1];
-            const uint32_t mn = vmin3(lo[o], lo[o + 1], lo[o + 2]), mx = vmax3(hi[o], hi[o + 1], hi[o + 2]);
-            uint32_t sflag = hfma_sat(hsub(mn, c), hsub(mx, c), F16_ONE);  // 1.0: noisy lane
-            const uint32_t dm = hsub(med, c);
-            out[o] = hfma(dm, sflag, c);
-            if constexpr (!FULL) {
-              const bool colok = x0 + o < valid_w;
-              sflag &= colok ? rowmask : 0u;
+            S[c] = tile::prmt(A[c], B[c], 0x5432u);  // rows y, y+1
+          lo[c] = vmin3(A[c], S[c], B[c]);
+          hi[c] = vmax3(A[c], S[c], B[c]);
+  #if IRDN_K3_MID_FMA
+          mid[c] = fma_sub(fma_sub(fma_add(B[c], one, fma_add(A[c], one, S[c])), m1, lo[c]), m1, hi[c]);
+  #else
+          mid[c] = A[c] + S[c] + B[c] - lo[c] - hi[c];
+  #endif
+          A[c] = B[c];
+        }
+        uint32_t rowmask = 0xFFFFFFFFu;  // partial tiles: lanes of rows inside the tile
+        if constexpr (MASKED) {
+          const int yr = y0 + 2 * s;
+          rowmask = (yr < valid_h ? 0x0000FFFFu : 0u) | (yr + 1 < valid_h ? 0xFFFF0000u : 0u);
+        }
+        uint32_t out[COLS];
+  #pragma unroll
+        for (int j = 0; j < COLS; j += 2) {
+          const uint32_t pm = vmin2(mid[j + 1], mid[j + 2]), qm = vmax2(mid[j + 1], mid[j + 2]);
+  #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int o = j + h;  // output column o: key columns o, o+1, o+2
+            const uint32_t md = vmax2(pm, vmin2(qm, mid[h == 0 ? j : j + 3]));
+            const uint32_t mxlo = vmax3(lo[o], lo[o + 1], lo[o + 2]);
+            const uint32_t mnhi = vmin3(hi[o], hi[o + 1], hi[o + 2]);
+            const uint32_t mn3 = vmin3(mxlo, md, mnhi), mx3 = vmax3(mxlo, md, mnhi);
+            uint32_t med;
+            if (IRDN_K3_FIN_FMA == 1 || (IRDN_K3_FIN_FMA == 2 && h == 1))
+              med = fma_sub(fma_sub(fma_add(mnhi, one, fma_add(mxlo, one, md)), m1, mn3), m1, mx3);
+            else
+              med = mxlo + md + mnhi - mn3 - mx3;
+            if constexpr (FNR) {
+              const uint32_t c = S[o + 1];
+              const uint32_t mn = vmin3(lo[o], lo[o + 1], lo[o + 2]), mx = vmax3(hi[o], hi[o + 1], hi[o + 2]);
+              uint32_t sflag = hfma_sat(hsub(mn, c), hsub(mx, c), F16_ONE);  // 1.0: noisy lane
+              const uint32_t dm = hsub(med, c);
+              out[o] = hfma(dm, sflag, c);
+              if constexpr (MASKED) {
+                const bool colok = x0 + o < valid_w;
+                sflag &= colok ? rowmask : 0u;
+              }
+              racc = hadd(racc, hmul_sat_abs(dm, sflag));
+              dacc = hadd(dacc, sflag);
+            } else {
+              out[o] = med;
             }
-            racc = hadd(racc, hmul_sat_abs(dm, sflag));
-            dacc = hadd(dacc, sflag);
-          } else {
-            out[o] = med;
           }
         }
-      }
-      // keys -> bytes: byte 0 of a key is the upper row's pixel, byte 2 the lower row's
-      uint32_t row_a[COLS / 4], row_b[COLS / 4];
-#pragma unroll
-      for (int w = 0; w < COLS / 4; ++w) {
-        const uint32_t q01 = tile::prmt(out[4 * w], out[4 * w + 1], 0x6240u);
-        const uint32_t q23 = tile::prmt(out[4 * w + 2], out[4 * w + 3], 0x6240u);
-        row_a[w] = tile::prmt(q01, q23, 0x5410u);
-        row_b[w] = tile::prmt(q01, q23, 0x7632u);
-      }
-      if constexpr (FULL) {
-        *reinterpret_cast<uint4*>(outp) = make_uint4(row_a[0], row_a[1], row_a[2], row_a[3]);
-        *reinterpret_cast<uint4*>(outp + p.out_pitch) = make_uint4(row_b[0], row_b[1], row_b[2], row_b[3]);
-      } else {
-        const int yr = y0 + 2 * s;
-        const uint8_t* ba = reinterpret_cast<const uint8_t*>(row_a);
-        const uint8_t* bb = reinterpret_cast<const uint8_t*>(row_b);
-        if (x0 + COLS <= valid_w) {
-          if (yr < valid_h) *reinterpret_cast<uint4*>(outp) = make_uint4(row_a[0], row_a[1], row_a[2], row_a[3]);
-          if (yr + 1 < valid_h)
-            *reinterpret_cast<uint4*>(outp + p.out_pitch) = make_uint4(row_b[0], row_b[1], row_b[2], row_b[3]);
+        // keys -> bytes: byte 0 of a key is the upper row's pixel, byte 2 the lower row's
+        uint32_t row_a[COLS / 4], row_b[COLS / 4];
+  #pragma unroll
+        for (int w = 0; w < COLS / 4; ++w) {
+          const uint32_t q01 = tile::prmt(out[4 * w], out[4 * w + 1], 0x6240u);
+          const uint32_t q23 = tile::prmt(out[4 * w + 2], out[4 * w + 3], 0x6240u);
+          row_a[w] = tile::prmt(q01, q23, 0x5410u);
+          row_b[w] = tile::prmt(q01, q23, 0x7632u);
+        }
+        if constexpr (!MASKED) {
+          *reinterpret_cast<uint4*>(outp) = make_uint4(row_a[0], row_a[1], row_a[2], row_a[3]);
+          *reinterpret_cast<uint4*>(outp + p.out_pitch) = make_uint4(row_b[0], row_b[1], row_b[2], row_b[3]);
         } else {
-#pragma unroll
-          for (int i = 0; i < COLS; ++i) {
-            if (x0 + i < valid_w) {
-              if (yr < valid_h) outp[i] = ba[i];
-              if (yr + 1 < valid_h) outp[p.out_pitch + i] = bb[i];
+          const int yr = y0 + 2 * s;
+          const uint8_t* ba = reinterpret_cast<const uint8_t*>(row_a);
+          const uint8_t* bb = reinterpret_cast<const uint8_t*>(row_b);
+          if (x0 + COLS <= valid_w) {
+            if (yr < valid_h) *reinterpret_cast<uint4*>(outp) = make_uint4(row_a[0], row_a[1], row_a[2], row_a[3]);
+            if (yr + 1 < valid_h)
+              *reinterpret_cast<uint4*>(outp + p.out_pitch) = make_uint4(row_b[0], row_b[1], row_b[2], row_b[3]);
+          } else {
+  #pragma unroll
+            for (int i = 0; i < COLS; ++i) {
+              if (x0 + i < valid_w) {
+                if (yr < valid_h) outp[i] = ba[i];
+                if (yr + 1 < valid_h) outp[p.out_pitch + i] = bb[i];
+              }
             }
           }
         }
+        outp += 2 * p.out_pitch;
       }
-      outp += 2 * p.out_pitch;
-    }
+    };
+    if (FULL || (ti.tx0 + TW <= p.width && ti.ty0 + G::TH <= p.row_end)) body(std::false_type{});
+    else if constexpr (!FULL) body(std::true_type{});
     if constexpr (FNR) {
       det_total += hsum_lanes(dacc);
       rep_total += hsum_lanes(racc);
