@@ -114,27 +114,69 @@ def _stats_from_native(s: _native.IrdnStats) -> FilterStats:
                        elapsed_ms=float(s.elapsed_ms), passes=int(s.passes))
 
 
-def _run(img, spec: WindowSpec, method: str, passes: int, device: int | None):
-    if not isinstance(spec, WindowSpec):
-        spec = WindowSpec(int(spec))
+def _as_spec(spec) -> WindowSpec:
+    """Any object with an odd `k` >= 3 (the reference's WindowSpec included), or an int."""
+    if isinstance(spec, WindowSpec):
+        return spec
+    return WindowSpec(int(getattr(spec, "k", spec)))
+
+
+def _is_gray_image(img) -> bool:
+    """GrayImage-shaped: width, height and a row-major pixel buffer (image.py:19-54) —
+    this package's GrayImage or the reference's own (duck-typed, no import of it)."""
+    return all(hasattr(img, a) for a in ("width", "height", "pixels")) and not isinstance(img, np.ndarray)
+
+
+def _run(img, spec, method: str, passes: int, device: int | None):
+    spec = _as_spec(spec)
     lib = _native.load_lib()
     m = _native.METHODS[method]
-    if isinstance(img, GrayImage):
-        n = img.width * img.height
-        src = (ctypes.c_char * n).from_buffer(img.pixels)
-        out = bytearray(n)
-        dst = (ctypes.c_char * n).from_buffer(out)
-        st = _native.IrdnStats()
-        _native.check(lib.irdn_run_filter_u8(ctypes.addressof(src), ctypes.addressof(dst), 1,
-                                             img.height, img.width, spec.k, m, passes,
-                                             device or 0, ctypes.byref(st)))
-        del src, dst
-        return GrayImage(img.width, img.height, out), _stats_from_native(st)
+    if _is_gray_image(img):
+        return _run_gray(lib, img, spec, m, passes, device or 0)
     if isinstance(img, np.ndarray):
         return _run_numpy(lib, img, spec, m, passes, device or 0)
     if type(img).__module__.startswith("torch"):
         return _run_torch(lib, img, spec, method, m, passes)
     raise TypeError(f"run_filter expects a GrayImage, numpy array or CUDA tensor, got {type(img)!r}")
+
+
+def _run_gray(lib, img, spec: WindowSpec, m: int, passes: int, device: int):
+    """GrayImage in, GrayImage of the same class out (filters.py:108 fresh buffer, :127).
+
+    8-bit images (bytes / bytearray / array('B') pixels) take irdn_run_filter_u8; a
+    duck-typed image with 16-bit pixels (array('H'), the reference's dtype-agnostic
+    per-window path) takes irdn_run_filter_u16."""
+    w, h = int(img.width), int(img.height)
+    if w < 1 or h < 1:
+        raise ValueError(f"image dimensions must be positive, got {w}x{h}")
+    src = np.frombuffer(img.pixels, dtype=np.uint16 if getattr(img.pixels, "itemsize", 1) == 2 else np.uint8)
+    if src.size != w * h:
+        raise ValueError(f"pixel buffer has {src.size} entries, expected {w * h}")
+    out = np.empty_like(src)
+    st = _native.IrdnStats()
+    fn = lib.irdn_run_filter_u8 if src.dtype == np.uint8 else lib.irdn_run_filter_u16
+    _native.check(fn(src.ctypes.data, out.ctypes.data, 1, h, w, spec.k, m, passes, device, ctypes.byref(st)))
+    if src.dtype == np.uint8:
+        pixels = bytearray(out.tobytes())
+    else:
+        from array import array
+
+        pixels = array("H", out.tobytes())
+    cls = type(img) if not isinstance(img, GrayImage) else GrayImage
+    try:
+        res = cls(w, h, pixels)
+    except Exception:
+        res = GrayImage(w, h, pixels) if src.dtype == np.uint8 else _PixelImage(w, h, pixels)
+    return res, _stats_from_native(st)
+
+
+@dataclass
+class _PixelImage:
+    """Result holder for a duck-typed 16-bit image whose class cannot be rebuilt."""
+
+    width: int
+    height: int
+    pixels: object
 
 
 def _shape3(shape) -> tuple[int, int, int]:

@@ -54,3 +54,14 @@ def cuda_ok():
 def cuda_ok_or_none():
     """True when a B200 is visible, False otherwise (never skips)."""
     return bool(gpu_available())
+
+
+@pytest.fixture(scope="session")
+def reference_pkg():
+    """The unmodified reference package (baseline/_ref, pip-installed from /root/reference)."""
+    from paper_1201_3972_b200 import launcher
+
+    try:
+        return launcher.import_reference()
+    except ImportError:
+        pytest.skip("the reference is not installed in baseline/_ref")

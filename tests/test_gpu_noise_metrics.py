@@ -16,7 +16,7 @@ from conftest import GOLDEN
 from oracle import oracle
 
 import paper_1201_3972_b200 as P
-from paper_1201_3972_b200 import _native, cli, metrics
+from paper_1201_3972_b200 import _native, launcher, metrics
 
 pytestmark = pytest.mark.gpu
 
@@ -107,9 +107,11 @@ def test_metrics_match_reference_goldens(cuda_ok):
         assert P.mse(a, b).hex() == m["mse"]  # numpy extension path
 
 
-def test_cli_end_to_end_matches_reference(cuda_ok, tmp_path, capsys):
-    """synth -> bench: the report rows equal the reference's (elapsed_ms aside);
-    add-noise and filter produce the reference's bytes and stats."""
+def test_cli_end_to_end_matches_reference(cuda_ok, tmp_path, capsys, reference_pkg):
+    """The UNMODIFIED reference CLI (baseline/_ref) with its filter re-pointed at the GPU by
+    reference_shim: synth -> bench report rows equal the reference's
+    (elapsed_ms aside); add-noise and filter produce the reference's bytes and stats."""
+    cli = launcher
     z = np.load(os.path.join(GOLDEN, "ref_metrics.npz"))
     rows_want = json.loads(str(z["meta"]))["rows"]
     clean = tmp_path / "clean.pgm"

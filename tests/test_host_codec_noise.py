@@ -1,5 +1,5 @@
 """CPU checks of the widened surface: PGM codec, fixtures, noise and
-metrics host logic, CLI plumbing — against goldens made by running the reference
+metrics host logic, the launcher over the reference CLI — against goldens made by running the reference
 (tests/golden/make_golden.py: ref_pgm.json, ref_noise.npz, ref_metrics.npz).
 
 The GPU halves (inject_impulse and the squared-error sums on the device) are in
@@ -20,7 +20,7 @@ from conftest import GOLDEN
 from oracle import oracle
 
 import paper_1201_3972_b200 as P
-from paper_1201_3972_b200 import cli, metrics
+from paper_1201_3972_b200 import launcher, metrics
 from paper_1201_3972_b200 import noise as N
 
 
@@ -166,7 +166,9 @@ def test_comparison_rows_match_reference(oracle_sums):
                                          metrics.MethodResult(2.0)).noisy.psnr_db)
 
 
-def test_cli_synth_and_errors(tmp_path, capsys):
+def test_cli_synth_and_errors(tmp_path, capsys, reference_pkg):
+    """The reference's own CLI through the launcher (the filter re-pointed by the shim)."""
+    cli = launcher
     out = tmp_path / "s.pgm"
     assert cli.main(["synth", "--fixture", "structured", "--output", str(out)]) == 0
     assert sha(P.read_pgm_file(out).pixels) == _pgm_golden()["fixtures"]["structured_128x128"]
