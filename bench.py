@@ -339,11 +339,12 @@ def _pyref_worker(args):
         im.width, im.height, im.pixels = w, h, array("H", crop.tobytes())
         spec = rimg.WindowSpec(k)
         st = rfil.FilterStats()
+        sc = rsort.SortCounters()
         for y in range(r_top, r_top + rows):
             for x in range(w):
                 win = rimg.extract_window(im, x, y, spec)
                 if rfil.classify_pixel(win, rfil.window_extrema(win, st)):
-                    rsort.median_of(win.values)
+                    rsort.median_of(win.values, sc)
     return rows * w, time.perf_counter() - t0
 
 
@@ -671,7 +672,7 @@ def time_gather(out, dev, rank: int, world: int, share: dict, cfg):
     import torch
     import torch.distributed as dist
 
-    flat = out.reshape(-1)
+    flat = out.reshape(-1).view(torch.uint8)  # bytes: gloo has no 16-bit integer collectives
     n = torch.tensor([flat.numel()], dtype=torch.int64, device=dev if _BACKEND == "nccl" else "cpu")
     sizes = [torch.empty_like(n) for _ in range(world)]
     dist.all_gather(sizes, n)
@@ -689,7 +690,7 @@ def time_gather(out, dev, rank: int, world: int, share: dict, cfg):
     dist.gather(send, bufs, dst=0)
     torch.cuda.synchronize(dev)
     secs = _max_over_ranks(time.perf_counter() - t0, dev)
-    bytes_in = sum(sizes) * out.element_size()
+    bytes_in = sum(sizes)
     return {"ms": round(secs * 1e3, 3), "bytes": bytes_in, "backend": _BACKEND,
             "note": "outputs stay sharded during the filter; this is one gather to rank 0, "
                     "not included in value"}

@@ -93,3 +93,55 @@ def test_b200_arm_passes2_and_widened_rows(cuda_ok):
         d = _run(["--path", path, "--steps", "10", "--warmup", "3", "--cpu-seconds", "1"])
         assert BASE_KEYS <= set(d) and d["value"] > 0 and d["roofline"]["unit"] == "GB/s"
         assert d["cpu_baseline"]["value"] > 0 and d["e2e"]["value"] > 0
+
+
+def test_reference_arm_under_torchrun_world2():
+    """Launched like the driver does for N > 1: rank 0 alone prints the line, the other
+    rank exits 0 without work; the config block names the N-GPU split."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(REPO, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--config", "c2", "--steps", "1", "--warmup", "1",
+           "--ref-seconds", "0.5"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=REPO)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["config"]["parallelism"].startswith("frame-sharded over 2 GPUs")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["c4", "c2"])
+def test_b200_arm_under_torchrun_world2(cuda_ok, config):
+    """Code-path check of the N-GPU split on a 1-GPU box (both ranks share the GPU, gloo
+    control plane): c4 as two row strips with halos, c2 as two frame shards; one line
+    from rank 0 with the separately timed gather. Not a scaling measurement."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(REPO, "bench.py"),
+           "--gpus", "2", "--config", config, "--steps", "20", "--warmup", "3", "--e2e-steps", "2"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=REPO)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["gather"]["bytes"] == d["run"]["pixels_per_step"] * (2 if d["dtype"] == "u16" else 1)
+    if config == "c4":
+        assert d["run"]["rank0_share"]["kind"] == "rows" and d["run"]["rank0_share"]["y1"] == 4096
+        assert d["config"]["parallelism"].startswith("row strips over 2 GPUs")
+    else:
+        assert d["run"]["rank0_share"] == {"kind": "frames", "f0": 0, "f1": 32, "replica": False}
+    assert d["e2e"]["value"] > 0

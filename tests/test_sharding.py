@@ -37,7 +37,29 @@ def test_band_bounds_match_reference_formula():
             assert b == [n * i // w for i in range(w + 1)]
 
 
-@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_strip_pass_plan_reads_only_fetched_rows():
+    """Every strip call of every pass reads rows the previous pass (or the fetched
+    strip) holds, produces a contiguous range, and counts exactly the owned rows."""
+    for height in (1, 7, 61):
+        for world in (1, 2, 3, 8, 70):
+            for k in (3, 5, 11):
+                for passes in (1, 2, 3):
+                    plan = sharding.shard_plan(1, height, world, k, passes)
+                    assert sum(sh.y1 - sh.y0 for sh in plan) == height
+                    for sh in plan:
+                        have = (sh.in0, sh.in1)
+                        for a, b, calls in sharding.strip_pass_plan(sh, height, k, passes):
+                            assert [c.row_begin for c in calls][0] == a and calls[-1].row_end == b
+                            assert all(x.row_end == y.row_begin for x, y in zip(calls, calls[1:]))
+                            assert sum(c.row_end - c.row_begin for c in calls if c.counted) == sh.y1 - sh.y0
+                            for c in calls:
+                                assert have[0] <= c.need0 and c.need1 <= have[1], (height, world, k, passes, sh)
+                            have = (a, b)
+                        if sh.y1 > sh.y0:
+                            assert have == (sh.y0, sh.y1)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8, 70])
 @pytest.mark.parametrize("k,passes,method", [(5, 1, "fnr"), (11, 1, "fnr"), (3, 2, "fnr"), (5, 2, "mf")])
 def test_row_strips_reassemble_exactly(world, k, passes, method):
     cfg = CONFIGS["c4"].with_shape(height=61, width=47)
@@ -121,22 +143,36 @@ def test_gloo_world2_matches_single_process(case):
 
 
 @pytest.mark.gpu
-def test_gpu_strip_plan_matches_whole_frame(cuda_ok):
+def test_gpu_device_shards_match_whole_frame(cuda_ok):
+    """The device executor (one H2D per shard, strip calls / one frame call on the GPU,
+    output left on the device) reassembles the single-GPU result for every rank count."""
+    import torch
+
     import paper_1201_3972_b200 as P
 
+    dev = torch.device("cuda", 0)
     cfg = CONFIGS["c4"].with_shape(height=1031, width=1280)
     img = generate(cfg, nframes=1)[0]
-    fn = sharding.cuda_strip_fn(0)
-    for passes in (1, 2):
-        whole, st = P.run_filter(img, P.WindowSpec(11), "fnr", passes)
+    for k, passes, method in ((11, 1, "fnr"), (11, 2, "fnr"), (5, 3, "mf")):
+        whole, st = P.run_filter(img, P.WindowSpec(k), method, passes)
         for world in (2, 3, 8):
             parts, tot = [], np.zeros(4, dtype=np.int64)
-            for sh in sharding.shard_plan(1, img.shape[0], world, 11, passes):
-                out, c = sharding.run_shard(img, sh, 11, "fnr", passes, fn)
-                parts.append(out)
+            for sh in sharding.shard_plan(1, img.shape[0], world, k, passes):
+                src = torch.from_numpy(np.ascontiguousarray(img[sh.in0:sh.in1]).view(np.int16)).to(dev)
+                out, c = sharding.run_shard_device(src, sh, img.shape[0], k, method, passes)
+                parts.append(out.cpu().numpy().view(np.uint16))
                 tot += c
-            assert np.array_equal(np.concatenate(parts), whole), (world, passes)
+            assert np.array_equal(np.concatenate(parts), whole), (k, passes, world)
             assert list(tot) == [st.minmax_scans, st.sorts, st.replacements, st.detected]
+    frames = generate(CONFIGS["c5"].with_shape(frames=7, height=96, width=128), nframes=7)
+    whole, st = P.run_filter(frames, P.WindowSpec(3), "fnr", 2)
+    parts, tot = [], np.zeros(4, dtype=np.int64)
+    for sh in sharding.shard_plan(7, 96, 3, 3, 2):
+        out, c = sharding.run_shard_device(torch.from_numpy(frames[sh.f0:sh.f1]).to(dev), sh, 96, 3, "fnr", 2)
+        parts.append(out.cpu().numpy())
+        tot += c
+    assert np.array_equal(np.concatenate(parts), whole)
+    assert list(tot) == [st.minmax_scans, st.sorts, st.replacements, st.detected]
 
 
 def _cuda_worker(rank, world, port, case, q):
