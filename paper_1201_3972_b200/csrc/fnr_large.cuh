@@ -137,9 +137,13 @@ __global__ void __launch_bounds__(THREADS) fnr_large_kernel(const T* __restrict_
     const T* frame = in + (int64_t)b * g.in_frame_stride;
     T* oframe = out + (int64_t)b * g.out_frame_stride;
     if (tid == 0) S.nq = 0;
-    // 1. halo tile, clamped against the global frame
+    // 1. halo tile, clamped against the global frame (replicate edge) and then to the rows
+    //    the input strip holds: rows past the strip only feed output rows past row_end of a
+    //    partial last tile, which are never stored, and must not be read (strip contract).
+    const int ylo = max(0, g.in_row0), yhi = min(g.height, g.in_row0 + g.in_rows) - 1;
     for (int iy = warp; iy < SH; iy += THREADS / 32) {
-      const T* src = frame + (int64_t)(clampi(y0 - r + iy, 0, g.height - 1) - g.in_row0) * g.in_pitch;
+      const int gy = clampi(clampi(y0 - r + iy, 0, g.height - 1), ylo, yhi);
+      const T* src = frame + (int64_t)(gy - g.in_row0) * g.in_pitch;
       for (int ix = lane; ix < SW; ix += 32) S.tile[iy * SW + ix] = src[clampi(x0 - r + ix, 0, g.width - 1)];
     }
     __syncthreads();

@@ -15,7 +15,7 @@
 //
 // One persistent kernel does it in a single pass (chained scan with decoupled
 // look-back): a CTA takes the next chunk of CHUNK draw positions in order (ticket),
-//   1. computes its 8192 draws (32 per thread: corruption + salt bit words),
+//   1. computes its CHUNK = 32768 draws (1024 threads x 32: corruption + salt bit words),
 //   2. composes the per-word functions (warp shuffles + one smem step) and publishes
 //      the chunk's function, then the whole CTA looks back over the predecessors'
 //      published functions / inclusive prefixes, 1024 chunks per step (one per thread:

@@ -18,9 +18,14 @@ import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 PEAK_ALU_LANES_PER_CLK_SM = 64  # measured, profiles/alu_probe_r01.txt
+HBM_PEAK_GBS = 6549.4  # MEASURED_PEAKS.json hbm_gbs on this pool
 
 
-UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+# ncu's raw page spells units several ways across versions ("msecond" / "ms", "Mbyte" / "MB");
+# round 1 missed the short forms, which printed a 1.16 ms launch as "1.2 us".
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1.0, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+        "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
+        "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
 
 
 def ncu_raw(rep: str) -> dict:
@@ -64,7 +69,7 @@ def launch_list(path: str) -> list[tuple[str, float]]:
             continue
         v = float(r[iv].replace(",", ""))
         unit = r[unit_i] if unit_i is not None else "nsecond"
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1e-3)
+        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}.get(unit, 1e-3)
         res.append((r[ik], v * scale))
     return res
 
@@ -84,6 +89,10 @@ def main():
         px = b["roofline"]["pixels_per_launch"]
         alg = b["roofline"]["algorithmic_bytes_per_launch"]
         dram = f(d, "dram__bytes_read.sum") + f(d, "dram__bytes_write.sum")  # bytes
+        # Writes that are still in the 126 MB L2 when the kernel ends never reach DRAM inside
+        # the capture, so DRAM writes undercount small outputs (c2: 3 of 42 MB). The L2 write
+        # sectors the SMs issued are the bytes the kernel wrote; report both.
+        l2w = f(d, "lts__t_sectors_srcunit_tex_op_write.sum") * 32.0
         dur_us = f(d, "gpu__time_duration.sum")
         alu_pct = f(d, "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active")
         issue_pct = f(d, "smsp__issue_active.avg.pct_of_peak_sustained_active")
@@ -95,6 +104,9 @@ def main():
         top = sorted(stalls.items(), key=lambda kv: -kv[1])[:5]
         launches = launch_list(os.path.join(src, f"launches_{cfg}.csv"))
         ours = [t for n, t in launches if "fnr_" in n]
+        # the profiled command also runs the chunked host-path (e2e) calls; the full-batch
+        # launches of the device-resident timed region are the long ones
+        full = [t for t in ours if ours and t > 0.5 * max(ours)]
         total = sum(t for _, t in launches)
         entry = {
             "tag": tag,
@@ -104,6 +116,8 @@ def main():
             "dram_read_bytes": f(d, "dram__bytes_read.sum"), "dram_write_bytes": f(d, "dram__bytes_write.sum"),
             "algorithmic_bytes_per_launch": alg,
             "traffic_over_algorithmic": (dram / alg) if dram == dram else None,
+            "l2_write_bytes": l2w if l2w == l2w else None,
+            "dram_read_plus_l2_write_bytes": (f(d, "dram__bytes_read.sum") + l2w) if l2w == l2w else None,
             "alu": {"bound": "alu", "pipe_utilisation_pct": alu_pct,
                     "thread_inst_per_px": inst * 32 / px,
                     "peak_lanes_per_clk_per_sm": PEAK_ALU_LANES_PER_CLK_SM,
@@ -111,7 +125,11 @@ def main():
             "issue_active_pct": issue_pct,
             "sm_clock_ghz_under_ncu": clk,
             "top_stalls": top,
-            "launch_list": {"filter_kernel_launches": len(ours),
+            "launch_list": {"full_batch_launches": len(full),
+                            "full_batch_mean_us": (sum(full) / len(full)) if full else None,
+                            "full_batch_hbm_frac": (alg / (sum(full) / len(full) * 1e-6) / 1e9 / HBM_PEAK_GBS)
+                            if full else None,
+                            "filter_kernel_launches": len(ours),
                             "filter_kernel_mean_us": (sum(ours) / len(ours)) if ours else None,
                             "share_of_gpu_time": (sum(ours) / total) if total else None},
             "bench": {"value_mpix_s": b["value"], "kernel_ms": b["roofline"]["kernel_ms"],
@@ -124,12 +142,15 @@ def main():
                  f"HBM frac {b['roofline']['frac']:.3f}, e2e {b['e2e']['value']:.0f} Mpix/s",
                  f"ncu: duration {dur_us:.1f} us (cold, serialised), DRAM {dram/1e6:.2f} MB "
                  f"(read {f(d, 'dram__bytes_read.sum')/1e6:.2f}, write {f(d, 'dram__bytes_write.sum')/1e6:.2f}; writes still "
-                 f"in the 126 MB L2 at kernel end are not counted) "
+                 f"in the 126 MB L2 at kernel end are not counted; L2 write sectors {l2w/1e6:.2f} MB) "
                  f"(algorithmic {alg/1e6:.2f} MB, ratio {entry['traffic_over_algorithmic']:.3f})",
                  f"ALU pipe {alu_pct:.1f}% of peak, issue active {issue_pct:.1f}%, "
                  f"{inst*32/px:.1f} thread-instructions / pixel, SM clock {clk:.2f} GHz",
                  "top stalls (warps per issue): " + ", ".join(f"{k} {v:.2f}" for k, v in top),
-                 f"launch list: {len(ours)} filter launches, mean {entry['launch_list']['filter_kernel_mean_us'] or 0:.1f} us, "
+                 f"launch list: {len(full)} full-batch launches, mean {entry['launch_list']['full_batch_mean_us'] or 0:.1f} us "
+                 f"(HBM frac {entry['launch_list']['full_batch_hbm_frac'] or 0:.3f}); "
+                 f"{len(ours)} filter launches in all (host-path chunks included), "
+                 f"mean {entry['launch_list']['filter_kernel_mean_us'] or 0:.1f} us, "
                  f"{100*(entry['launch_list']['share_of_gpu_time'] or 0):.1f}% of GPU time in the profiled run"]
         open(os.path.join(REPO, "profiles", f"ncu_{tag}_{cfg}.txt"), "w").write("\n".join(lines) + "\n")
         table.append(f"| {cfg} | {b['value']:.0f} | {b['roofline']['kernel_ms']*1e3:.1f} | {b['roofline']['frac']:.3f} | "
