@@ -18,7 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CUDA_SOURCES = ["irdn_api.cu", "delta_host.cpp"]
 CUDA_HEADERS = ["fnr_common.cuh", "fnr_generic.cuh", "fnr_fast.cuh", "fnr_tile.cuh",
-                "select_nets.cuh", "fnr_k3.cuh", "fnr_warp.cuh", "noise.cuh", "metrics.cuh", "delta.cuh", "fnr_large.cuh"]
+                "select_nets.cuh", "sep_nets.cuh", "fnr_dense.cuh", "fnr_k3.cuh", "fnr_warp.cuh", "noise.cuh", "metrics.cuh", "delta.cuh", "fnr_large.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,0 +1,165 @@
+// Dense median stage of the warp kernel (fnr_warp.cuh) for k = 5 and 7: the median of
+// EVERY pixel of a warp tile from shared sorted rows, for MF (reference filters.py:179-180)
+// and for FNR tiles where many pixels are flagged (filters.py:172-176: 49 % of c3's).
+//
+// The queue path pays a full k*k selection network per flagged pixel (7x7: 514 VIMNMX
+// per two pixels) plus a k*k gather. Here each lane walks its column pair (one u16x2
+// word per row: two horizontally adjacent pixels) down the tile and
+//   1. sorts each window ROW once (the k values at columns x-r .. x+r of one row, for both
+//      pixels of the pair: the detector's word loads plus PRMT/IMAD-shifted odd offsets),
+//   2. merges sorted rows into blocks that vertically adjacent outputs share, pruned to the
+//      ranks that can still be the median (sep_nets.cuh, generated and checked by
+//      tools/netgen/sepgen.py; structure after Adams, "Fast median filters using separable
+//      sorting networks", 2021):
+//        k = 7, output rows a..a+3:  P = pairs of sorted rows, C4 = rows a..a+3 (ranks 3..24),
+//              C6 = C4 + the pair above / below (ranks 17..24), median = rank 7 of C6 + 1 row
+//        k = 5, output rows a, a+1:  C4 = rows a-1..a+2 (ranks 7..12), median = rank 5 of C4 + 1 row
+//      60.75 (k = 7) / 28 (k = 5) VIMNMX instructions per pixel instead of 257 / 86 per
+//      queued pixel;
+//   3. stores the medians of the flagged pixels (FNR; the detector already stored the
+//      others) or of all pixels (MF), and counts replacements (median != centre).
+// The median is a selected input value, so the result is bit-identical to the introsort's.
+#pragma once
+#include "sep_nets.cuh"
+
+namespace irdn {
+namespace wk {
+
+// Sorted window row of smem row `rowp` (pointing at the lane's first pixel): v[i] is the
+// i-th smallest of the k values around each pixel of the pair (u16x2 lanes).
+template <typename T, int K>
+__device__ __forceinline__ void sorted_row(const T* rowp, uint32_t (&v)[K], uint32_t k65536) {
+  constexpr int r = K / 2, J = (r + 1) / 2;
+  uint32_t wd[2 * J + 1];
+#pragma unroll
+  for (int j = -J; j <= J; ++j) wd[j + J] = tile::load_pair<T>(rowp, 2 * j);
+#pragma unroll
+  for (int d = -r; d <= r; ++d)
+    v[d + r] = (d & 1) == 0 ? wd[J + d / 2] : shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536);
+  if constexpr (K == 7) sep::sort7(v);
+  else sep::sort5(v);
+}
+
+// Store the medians `med` of output row y (tile coordinates): FNR stores only the flagged
+// pixels (flag bits: row y at bit y % 16 and 16 + y % 16 of flags[y / 16], already masked
+// to the valid part of the tile) and counts the ones that change; MF stores every valid one.
+template <typename T>
+__device__ __forceinline__ uint32_t put_row(T* rowp, const T* crow, uint32_t med, int y, int valid_rows, bool ok0,
+                                            bool ok1, const uint32_t (&flags)[2], bool fnr) {
+  if (!fnr) {
+    if (y < valid_rows) tile::store_pair_g<T>(rowp, med, ok0, ok1);
+    return 0u;
+  }
+  const uint32_t f = flags[y >> 4] >> (y & 15);
+  const bool f0 = f & 1u, f1 = (f >> 16) & 1u;
+  if (!(f0 | f1)) return 0u;
+  const uint32_t c = tile::load_pair<T>(crow, 0);
+  const uint32_t lo = med & 0xFFFFu, hi = med >> 16;
+  uint32_t rep = 0;
+  if (f0 && f1) {
+    tile::store_pair_g<T>(rowp, med, true, true);
+  } else if (f0) {
+    rowp[0] = (T)lo;
+  } else {
+    rowp[1] = (T)hi;
+  }
+  rep += (f0 && lo != (c & 0xFFFFu)) + (f1 && hi != (c >> 16));
+  return rep;
+}
+
+// Dense medians of one warp tile (rows 0 .. rows-1, rows a multiple of the group size);
+// k = 5 or 7 only (other windows never call it: wk::kDense).
+// s_in: the staged box (box row b = tile row b - r); c0: smem column of the lane's first
+// pixel; outp: output pixel (0, 2 * lane) of the tile. Returns the replacements (FNR).
+template <typename T, int K, int BOXW>
+__device__ __forceinline__ uint32_t dense_tile(const T* s_in, int c0, T* outp, int64_t pitch, int rows,
+                                               int valid_rows, bool ok0, bool ok1, const uint32_t (&flags)[2],
+                                               bool fnr, uint32_t k65536) {
+  constexpr int r = K / 2;
+  const T* base = s_in + c0 + r * BOXW;  // window row q of the tile = base + q * BOXW
+  uint32_t replaced = 0;
+  auto S = [&](int q, uint32_t (&v)[K]) {
+    if constexpr (K == 5 || K == 7) sorted_row<T, K>(base + q * BOXW, v, k65536);
+  };
+  auto put = [&](int y, uint32_t med) {
+    replaced += put_row<T>(outp + (int64_t)y * pitch, base + y * BOXW, med, y, valid_rows, ok0, ok1, flags, fnr);
+  };
+  if constexpr (K == 7) {
+    // state at group a: Pm2 = P[a-2], P0 = P[a], Sm3 = S[a-3], Sm1 = S[a-1], S1 = S[a+1], S2 = S[a+2]
+    uint32_t Pm2[14], P0[14], Sm3[7], Sm1[7], S1[7], S2[7];
+    {
+      uint32_t t[7];
+      S(-3, Sm3);
+      S(-2, t);
+      S(-1, Sm1);
+      sep::merge7(t, Sm1, Pm2);
+      S(0, t);
+      S(1, S1);
+      sep::merge7(t, S1, P0);
+      S(2, S2);
+    }
+#pragma unroll 1
+    for (int a = 0; a < rows; a += 4) {
+      uint32_t S3[7], S4[7], S5[7], S6[7], P2[14], P4[14];
+      S(a + 3, S3);
+      S(a + 4, S4);
+      S(a + 5, S5);
+      S(a + 6, S6);
+      sep::merge7(S2, S3, P2);
+      sep::merge7(S4, S5, P4);
+      uint32_t c4[22], cA[8], cB[8];
+      sep::core4_7(P0, P2, c4);
+      sep::core6_7(c4, Pm2, cA);
+      sep::core6_7(c4, P4, cB);
+      put(a, sep::final7(cA, Sm3));
+      put(a + 1, sep::final7(cA, S4));
+      put(a + 2, sep::final7(cB, Sm1));
+      put(a + 3, sep::final7(cB, S6));
+#pragma unroll
+      for (int i = 0; i < 14; ++i) {
+        Pm2[i] = P2[i];
+        P0[i] = P4[i];
+      }
+#pragma unroll
+      for (int i = 0; i < 7; ++i) {
+        Sm3[i] = S1[i];
+        Sm1[i] = S3[i];
+        S1[i] = S5[i];
+        S2[i] = S6[i];
+      }
+    }
+  } else if constexpr (K == 5) {
+    // state at group a: Pm1 = P[a-1], Sm2 = S[a-2], S0 = S[a], S1 = S[a+1]
+    uint32_t Pm1[10], Sm2[5], S0[5], S1[5];
+    {
+      uint32_t t[5];
+      S(-2, Sm2);
+      S(-1, t);
+      S(0, S0);
+      sep::merge5(t, S0, Pm1);
+      S(1, S1);
+    }
+#pragma unroll 1
+    for (int a = 0; a < rows; a += 2) {
+      uint32_t S2[5], S3[5], P1[10], c[6];
+      S(a + 2, S2);
+      S(a + 3, S3);
+      sep::merge5(S1, S2, P1);
+      sep::core4_5(Pm1, P1, c);
+      put(a, sep::final5(c, Sm2));
+      put(a + 1, sep::final5(c, S3));
+#pragma unroll
+      for (int i = 0; i < 10; ++i) Pm1[i] = P1[i];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        Sm2[i] = S0[i];
+        S0[i] = S2[i];
+        S1[i] = S3[i];
+      }
+    }
+  }
+  return replaced;
+}
+
+}  // namespace wk
+}  // namespace irdn

@@ -156,6 +156,20 @@ inline int sm_count(int dev) {
 // made inside a CUDA-graph capture still works. Streams beyond kSchedSlots per device
 // share slots round-robin (not expected: one slot per concurrently used stream).
 constexpr int kSchedSlots = 256;
+
+// Warp kernel, k = 5 / 7: flagged pixels per 64 x 32 tile above which the tile takes the
+// dense median stage (fnr_dense.cuh) instead of the per-pixel queue; MF is always dense.
+// The crossover is where the queue's per-pixel network (plus gather) costs as much as
+// the dense stage does for the whole tile. IRDN_DENSE_FRAC overrides
+// the fraction (A/B experiments; < 0 disables the dense stage, MF included).
+template <int K>
+inline int dense_min_for() {
+  if (K != 5 && K != 7) return -1;
+  static const double env = getenv("IRDN_DENSE_FRAC") ? atof(getenv("IRDN_DENSE_FRAC")) : -2.0;
+  const double frac = env > -2.0 ? env : (K == 7 ? 0.22 : 0.30);
+  if (frac < 0.0) return -1;
+  return (int)(frac * wk::WW * wk::WH);
+}
 inline unsigned int* sched_slot(int dev, cudaStream_t s) {
   struct Entry { int dev; cudaStream_t s; unsigned int slot; };
   static std::mutex mu;
@@ -227,6 +241,7 @@ inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.counts = counts;
   p.sched = sched;
   p.one = 1u;
+  p.dense_min = -1;
   p.debug = getenv("IRDN_DEBUG") ? atoi(getenv("IRDN_DEBUG")) : 0;
   p.full_tiles = 0;
   p.static_rounds = 0;
@@ -293,6 +308,7 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.counts = counts;
   p.sched = sched;
   p.one = 1u;
+  p.dense_min = dense_min_for<K>();
   p.debug = 0;
   p.debug_buf = nullptr;
 #ifdef IRDN_TIMELINE
@@ -420,6 +436,7 @@ inline int launch_warp_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, 
   p.counts = counts;
   p.sched = sched;
   p.one = 1u;
+  p.dense_min = dense_min_for<K>();
   p.debug = 0;
   p.debug_buf = nullptr;
   p.passes = passes;
@@ -537,6 +554,7 @@ inline int launch_k3_kern(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g
   p.counts = counts;
   p.sched = sched;
   p.one = 1u;
+  p.dense_min = -1;
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));

@@ -92,6 +92,9 @@ struct TileParams {
   unsigned int* flags;    // [0] launch epoch of the stream; from [32]: (passes - 1) x tiles-per-pass flags
   uint32_t epoch;         // unused on the host (the kernel derives the epoch from flags[0])
   unsigned long long* debug_buf;  // experiments only (IRDN_TIMELINE builds): per-warp timeline
+  // warp kernel, k = 5 / 7 (fnr_dense.cuh): FNR tiles with more than dense_min flagged
+  // pixels take the dense median stage; dense_min < 0 keeps MF on the queue path too
+  int32_t dense_min;
 };
 
 // ---- PTX helpers ------------------------------------------------------------

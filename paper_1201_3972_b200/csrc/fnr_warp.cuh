@@ -16,9 +16,15 @@
 // nearest in-frame cell (replicate edge, image.py:117-130) before filtering.
 #pragma once
 #include "fnr_tile.cuh"
+#include "fnr_dense.cuh"
 
 namespace irdn {
 namespace wk {
+
+// Windows with a dense-median stage (fnr_dense.cuh): MF always (unless p.dense_min < 0),
+// FNR for tiles with more than p.dense_min flagged pixels.
+template <int K>
+constexpr bool kDense = K == 5 || K == 7;
 
 #ifndef IRDN_WARPS
 #define IRDN_WARPS 2
@@ -451,7 +457,16 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
       detected += (uint32_t)cnt;
       const int off = incl - cnt;  // index of this lane's first queue entry
       const uint32_t ebase = (uint32_t)(2 * lane);
-      for (int q0 = 0; q0 < n; q0 += QCAP) {
+      bool dense = false;
+      if constexpr (kDense<K>) {
+        // many flagged pixels: every pixel's median from shared sorted rows (fnr_dense.cuh)
+        if (p.dense_min >= 0 && n * WH > p.dense_min * ti.rows) {  // dense_min: per full-height tile
+          dense = true;
+          replaced += dense_tile<T, K, BOXW>(s_in, c0, out_tile + 2 * lane, p.out_pitch, ti.rows, valid_h, ok0,
+                                             ok1, flags, true, p.one << 16);
+        }
+      }
+      for (int q0 = 0; q0 < (dense ? 0 : n); q0 += QCAP) {
         if (off < q0 + QCAP && off + cnt > q0) {
           int idx = off - q0;
 #pragma unroll
@@ -470,6 +485,11 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
         replaced += medians<T, K>(s_in, s_q, min(QCAP, n - q0), out_tile, p.out_pitch, lane, true, 0u - p.one);
         __syncwarp();  // queue reads done before the next round overwrites it
       }
+    } else if (kDense<K> && p.dense_min >= 0) {
+      const uint32_t none[2] = {0u, 0u};
+      n = valid_h * valid_w;
+      dense_tile<T, K, BOXW>(s_in, c0, out_tile + 2 * lane, p.out_pitch, ti.rows, valid_h, ok0, ok1, none, false,
+                             p.one << 16);
     } else {
       const int cols = max(0, valid_w), rows = max(0, valid_h);
       n = rows * cols;
