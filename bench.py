@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--method", default="fnr", choices=["fnr", "mf"],
+                    help="filter method (run_filter's `method`); the metric is quoted on fnr")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="CPU-baseline sample budget (seconds of single-core oracle work)")
     ap.add_argument("--ref-seconds", type=float, default=4.0,
@@ -124,10 +126,10 @@ def scaling_kind(cfg, world: int) -> str:
     return "weak" if (cfg.name == "c1" and world > 1) else "strong"
 
 
-def config_block(cfg, world: int, passes: int) -> dict:
+def config_block(cfg, world: int, passes: int, method: str = "fnr") -> dict:
     """Identical in both arms (the driver compares the arms' config)."""
     return {"workload": f"{cfg.name}: {cfg.description}", "frames": cfg.frames, "height": cfg.height,
-            "width": cfg.width, "dtype": cfg.dtype, "k": cfg.k, "method": "fnr", "passes": passes,
+            "width": cfg.width, "dtype": cfg.dtype, "k": cfg.k, "method": method, "passes": passes,
             "parallelism": parallelism(cfg, world)}
 
 
@@ -148,9 +150,14 @@ def job_pixels(cfg, world: int) -> int:
 #     (K-1)(1 + 2r/32) horizontal + (K-1) vertical + 1 flag test per pair, plus the median
 #     network for two flagged pixels (select_nets.cuh) times the detected fraction.
 NET_INSTR_PER_PAIR = {3: 30, 5: 172, 7: 514, 9: None, 11: 1833}
+# dense median stage (fnr_dense.cuh, sep_nets.cuh; k = 5 / 7): VIMNMX instructions per output
+# pair (tools/netgen/sepgen.py prints them), taken by MF always and by FNR tiles whose
+# flagged fraction exceeds DENSE_FRAC (fnr_fast.cuh dense_min_for)
+DENSE_INSTR_PER_PAIR = {5: 56.0, 7: 121.5}
+DENSE_FRAC = {5: 0.30, 7: 0.22}
 
 
-def static_ops(cfg, detected_fraction: float) -> dict:
+def static_ops(cfg, detected_fraction: float, method: str = "fnr") -> dict:
     if cfg.k == 3 and cfg.dtype == "u8":
         per_pair = 2 * 18 / 16 + 4 + 3 + 2
         return {"method": "dense sorted-columns 3x3 median + extremum detector (every pixel)",
@@ -160,6 +167,14 @@ def static_ops(cfg, detected_fraction: float) -> dict:
     K, r = cfg.k, cfg.k // 2
     det = (K - 1) * (1 + 2 * r / 32) + (K - 1) + 1
     net = NET_INSTR_PER_PAIR.get(K)
+    dense = DENSE_INSTR_PER_PAIR.get(K)
+    if dense is not None and (method == "mf" or detected_fraction > DENSE_FRAC[K]):
+        per_pair = dense + (det if method == "fnr" else 0.0)
+        return {"method": f"separable {K}x{K} median of every pixel pair from shared sorted rows "
+                          f"({dense} instructions per two medians)"
+                          + (" + extremum detector" if method == "fnr" else ""),
+                "minmax_instr_per_px": round(per_pair / 2, 3), "minmax_lane_ops_per_px": round(per_pair, 3),
+                "detected_fraction": round(detected_fraction, 4)}
     per_pair = det + (net or 0) * detected_fraction
     return {"method": f"separable {K}x{K} extremum detector on every pixel pair + generated selection "
                       f"network on the flagged pairs ({net} instructions per two medians)",
@@ -291,7 +306,7 @@ def _gather_sum(values: list[int], dev) -> list[int]:
 # ---------------------------------------------------------------------------
 # CPU legs (oracle = the reference algorithm restated in C; test/baseline only)
 # ---------------------------------------------------------------------------
-def cpu_sample_run(cfg, frames: np.ndarray, budget_s: float):
+def cpu_sample_run(cfg, frames: np.ndarray, budget_s: float, method: str = "fnr"):
     """One-thread oracle port over a bounded sample; returns (pixels, seconds, description)."""
     from oracle import oracle
 
@@ -308,7 +323,7 @@ def cpu_sample_run(cfg, frames: np.ndarray, budget_s: float):
     else:
         n = 0
         while time.perf_counter() - t0 < budget_s and n < frames.shape[0]:
-            oracle.run_filter_c(frames[n], cfg.k, "fnr", 1, threads=1)
+            oracle.run_filter_c(frames[n], cfg.k, method, 1, threads=1)
             px += cfg.height * cfg.width
             n += 1
         desc = f"{n} frame(s) of {cfg.height}x{cfg.width} {cfg.dtype}"
@@ -413,14 +428,14 @@ def run_reference_arm(args, cfg, rank: int, world: int):
     else:
         probe = generate(cfg, nframes=1, lib=olib)
         t0 = time.perf_counter()
-        oracle.run_filter_c(probe, cfg.k, "fnr", 1, threads=threads)
+        oracle.run_filter_c(probe, cfg.k, args.method, 1, threads=threads)
         dt = time.perf_counter() - t0
         nfr = int(max(1, min(cfg.frames, math.ceil(1.0 / max(dt, 1e-4)))))
         frames = generate(cfg, nframes=nfr, lib=olib)
         sample_frames = frames
 
         def step():
-            oracle.run_filter_c(frames, cfg.k, "fnr", 1, threads=threads)
+            oracle.run_filter_c(frames, cfg.k, args.method, 1, threads=threads)
             return nfr * cfg.height * cfg.width
         sample = f"{nfr} of {cfg.frames} frame(s) {cfg.height}x{cfg.width} {cfg.dtype} per step, {threads} threads (row bands)"
     for _ in range(args.warmup):
@@ -437,7 +452,7 @@ def run_reference_arm(args, cfg, rank: int, world: int):
         "n_gpus": world, "steps": steps, "warmup": args.warmup,
         "ms_per_step": round(dt / steps * 1e3, 3), "higher_is_better": True, "scaling": scaling_kind(cfg, world),
         "vs_baseline": None, "dtype": cfg.dtype, "data": DATA,
-        "config": config_block(cfg, world, 1),
+        "config": config_block(cfg, world, 1, args.method),
         "cpu_baseline": {"value": round(value, 4), "unit": "Mpix/s", "cores": threads, "kind": "port",
                          "sample": sample,
                          "note": "oracle/fnr_oracle.c: C restatement of the reference's run_filter "
@@ -496,6 +511,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
     sptr = stream.cuda_stream
     t = "u8" if bpp == 1 else "u16"
     fpass = getattr(lib, f"irdn_filter_pass_{t}")
+    M = _native.METHODS[args.method]
     fdev = getattr(lib, f"irdn_run_filter_device_{t}")
     fstrip = getattr(lib, f"irdn_filter_strip_{t}")
 
@@ -503,11 +519,11 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
         src, dst = ins[i % R].data_ptr(), outs[i % R].data_ptr()
         if share["kind"] == "rows":
             rc = fstrip(src, share["in0"], share["in1"] - share["in0"], dst, share["y0"], share["y1"], H, W, W, W,
-                        cfg.k, 0, counts.data_ptr(), sptr)
+                        cfg.k, M, counts.data_ptr(), sptr)
         elif passes == 1:
-            rc = fpass(src, dst, B, H, W, W, W, cfg.k, 0, counts.data_ptr(), sptr)
+            rc = fpass(src, dst, B, H, W, W, W, cfg.k, M, counts.data_ptr(), sptr)
         else:  # run_filter over device buffers: passes back-to-back launches through tmp
-            rc = fdev(src, dst, tmp.data_ptr(), B, H, W, cfg.k, 0, passes, counts.data_ptr(), sptr)
+            rc = fdev(src, dst, tmp.data_ptr(), B, H, W, cfg.k, M, passes, counts.data_ptr(), sptr)
         if rc != 0:
             _native.check(rc)
 
@@ -605,7 +621,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
                 "kernel_ms_source": "CUDA events on the launching stream over the timed region / filter launches",
                 "kernel_ms_isolated": round(statistics.mean(per), 5),
                 "kernel_ms_isolated_min": round(min(per), 5),
-                "static_ops": static_ops(cfg, det_rank / max(1, rank_px * steps * passes))}
+                "static_ops": static_ops(cfg, det_rank / max(1, rank_px * steps * passes), args.method)}
     if prof.get("instr_per_px"):
         # SM-side floors from the committed capture (instructions / ALU-pipe instructions per pixel)
         ipp, app = prof["instr_per_px"], prof.get("alu_instr_per_px")
@@ -632,7 +648,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
         from oracle import oracle
 
         oracle.lib()
-        px, secs, desc = cpu_sample_run(cfg, host, args.cpu_seconds)
+        px, secs, desc = cpu_sample_run(cfg, host, args.cpu_seconds, args.method)
         cpu = {"value": round(px / secs / 1e6, 4), "unit": "Mpix/s", "cores": 1, "kind": "port",
                "sample": desc + f" ({secs:.1f} s)",
                "note": "oracle/fnr_oracle.c (reference algorithm restated in C: clamp gather, "
@@ -644,7 +660,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
             "steps": steps, "warmup": warmup, "ms_per_step": round(ms_per_step, 5),
             "higher_is_better": True, "scaling": scaling_kind(cfg, world), "vs_baseline": None,
             "dtype": cfg.dtype, "data": DATA,
-            "config": config_block(cfg, world, passes),
+            "config": config_block(cfg, world, passes, args.method),
             "run": {"pixels_per_step": job_pixels(cfg, world), "rank0_share": share,
                     "detected_per_step": det_total // steps,
                     "l2": f"rotating {R} distinct in/out buffers ({(in_bytes + rank_px * bpp) * R / 1e6:.0f} MB > 2x L2)"
@@ -704,6 +720,7 @@ def run_e2e(args, cfg, lib, _native, h_in, d_out_ref, share, steps, dev, world, 
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(steps, 10 if h_in.numel() * bpp > (256 << 20) else 40))
     t = "u8" if bpp == 1 else "u16"
     H, W = cfg.height, cfg.width
+    M = _native.METHODS[args.method]
     if share["kind"] == "rows":
         # a row strip: H2D of the strip (+ halo rows), irdn_filter_strip_*, D2H of the owned rows
         fstrip = getattr(lib, f"irdn_filter_strip_{t}")
@@ -717,7 +734,7 @@ def run_e2e(args, cfg, lib, _native, h_in, d_out_ref, share, steps, dev, world, 
         def call():
             d_in.copy_(h_in, non_blocking=True)
             _native.check(fstrip(d_in.data_ptr(), share["in0"], share["in1"] - share["in0"], d_out.data_ptr(),
-                                 share["y0"], share["y1"], H, W, W, W, cfg.k, 0, counts.data_ptr(), s.cuda_stream))
+                                 share["y0"], share["y1"], H, W, W, W, cfg.k, M, counts.data_ptr(), s.cuda_stream))
             h_out.copy_(d_out, non_blocking=True)
             s.synchronize()
         call()
@@ -743,12 +760,12 @@ def run_e2e(args, cfg, lib, _native, h_in, d_out_ref, share, steps, dev, world, 
     st = _native.IrdnStats()
     hfn = getattr(lib, f"irdn_run_filter_{t}")
     for _ in range(2):
-        _native.check(hfn(h_in.data_ptr(), h_out.data_ptr(), B, H, W, cfg.k, 0, passes, local, ctypes.byref(st)))
+        _native.check(hfn(h_in.data_ptr(), h_out.data_ptr(), B, H, W, cfg.k, M, passes, local, ctypes.byref(st)))
 
     def e2e_run(mode: str):
         prev = _native.set_host_return(mode)
         try:
-            _native.check(hfn(h_in.data_ptr(), h_out.data_ptr(), B, H, W, cfg.k, 0, passes, local,
+            _native.check(hfn(h_in.data_ptr(), h_out.data_ptr(), B, H, W, cfg.k, M, passes, local,
                               ctypes.byref(st)))
             if world > 1:
                 import torch.distributed as dist
@@ -756,7 +773,7 @@ def run_e2e(args, cfg, lib, _native, h_in, d_out_ref, share, steps, dev, world, 
                 dist.barrier()
             t0 = time.perf_counter()
             for _ in range(e2e_steps):
-                _native.check(hfn(h_in.data_ptr(), h_out.data_ptr(), B, H, W, cfg.k, 0, passes, local,
+                _native.check(hfn(h_in.data_ptr(), h_out.data_ptr(), B, H, W, cfg.k, M, passes, local,
                                   ctypes.byref(st)))
             secs = time.perf_counter() - t0
             if world > 1:

@@ -71,18 +71,39 @@ __device__ __forceinline__ uint32_t put_row(T* rowp, const T* crow, uint32_t med
 // k = 5 or 7 only (other windows never call it: wk::kDense).
 // s_in: the staged box (box row b = tile row b - r); c0: smem column of the lane's first
 // pixel; outp: output pixel (0, 2 * lane) of the tile. Returns the replacements (FNR).
-template <typename T, int K, int BOXW>
+//
+// FUSED (FNR on a whole tile that is predicted dense, i.e. the detector did not run): the
+// detector comes from the same sorted rows — a window's min / max is the min / max of its
+// rows' first / last sorted elements, shared between the rows of a group — and every pixel
+// is stored once as  noisy ? median : centre  (branch-free on packed words:
+// m = min(c - min, max - c) is 0 exactly in noisy lanes). *detected receives the tile's
+// noisy pixels (whole tiles only: no row / column masking).
+template <typename T, int K, int BOXW, bool FUSED = false>
 __device__ __forceinline__ uint32_t dense_tile(const T* s_in, int c0, T* outp, int64_t pitch, int rows,
                                                int valid_rows, bool ok0, bool ok1, const uint32_t (&flags)[2],
-                                               bool fnr, uint32_t k65536) {
+                                               bool fnr, uint32_t one, uint32_t* detected = nullptr) {
   constexpr int r = K / 2;
+  const uint32_t k65536 = one << 16, m1 = 0u - one;
+  const uint32_t ones = one * 0x00010001u, kffff = one * 0xFFFFu;
   const T* base = s_in + c0 + r * BOXW;  // window row q of the tile = base + q * BOXW
   uint32_t replaced = 0;
+  uint32_t sacc = 0, racc = 0;  // FUSED: per-lane counts of signal / replaced pixels (u16 lanes, <= rows)
   auto S = [&](int q, uint32_t (&v)[K]) {
     if constexpr (K == 5 || K == 7) sorted_row<T, K>(base + q * BOXW, v, k65536);
   };
   auto put = [&](int y, uint32_t med) {
     replaced += put_row<T>(outp + (int64_t)y * pitch, base + y * BOXW, med, y, valid_rows, ok0, ok1, flags, fnr);
+  };
+  // FUSED store of output row y: window min mn, max mx
+  auto put_f = [&](int y, uint32_t med, uint32_t mn, uint32_t mx) {
+    const uint32_t c = tile::load_pair<T>(base + y * BOXW, 0);
+    const uint32_t m = vmin2(fma_sub(c, m1, mn), fma_sub(mx, m1, c));  // lane 0 <=> noisy
+    const uint32_t z = vmin2(m, ones);                                  // 1 signal, 0 noisy
+    const uint32_t keep = fma_add(z, kffff, 0u);                        // 0xFFFF in signal lanes
+    const uint32_t out = (c & keep) | (med & ~keep);
+    tile::store_pair_g<T>(outp + (int64_t)y * pitch, out, true, true);
+    sacc = fma_add(z, one, sacc);
+    racc = fma_add(vmin2(out ^ c, ones), one, racc);
   };
   if constexpr (K == 7) {
     // state at group a: Pm2 = P[a-2], P0 = P[a], Sm3 = S[a-3], Sm1 = S[a-1], S1 = S[a+1], S2 = S[a+2]
@@ -111,10 +132,19 @@ __device__ __forceinline__ uint32_t dense_tile(const T* s_in, int c0, T* outp, i
       sep::core4_7(P0, P2, c4);
       sep::core6_7(c4, Pm2, cA);
       sep::core6_7(c4, P4, cB);
-      put(a, sep::final7(cA, Sm3));
-      put(a + 1, sep::final7(cA, S4));
-      put(a + 2, sep::final7(cB, Sm1));
-      put(a + 3, sep::final7(cB, S6));
+      if constexpr (FUSED) {
+        // window rows: a-3 | a-2, a-1 | a .. a+3 (shared) | a+4 | a+5 | a+6
+        const uint32_t tn = vmin2(P0[0], P2[0]), tx = vmax2(P0[13], P2[13]);
+        put_f(a, sep::final7(cA, Sm3), vmin3(tn, Sm3[0], Pm2[0]), vmax3(tx, Sm3[6], Pm2[13]));
+        put_f(a + 1, sep::final7(cA, S4), vmin3(tn, Pm2[0], S4[0]), vmax3(tx, Pm2[13], S4[6]));
+        put_f(a + 2, sep::final7(cB, Sm1), vmin3(tn, Sm1[0], P4[0]), vmax3(tx, Sm1[6], P4[13]));
+        put_f(a + 3, sep::final7(cB, S6), vmin3(tn, P4[0], S6[0]), vmax3(tx, P4[13], S6[6]));
+      } else {
+        put(a, sep::final7(cA, Sm3));
+        put(a + 1, sep::final7(cA, S4));
+        put(a + 2, sep::final7(cB, Sm1));
+        put(a + 3, sep::final7(cB, S6));
+      }
 #pragma unroll
       for (int i = 0; i < 14; ++i) {
         Pm2[i] = P2[i];
@@ -146,8 +176,15 @@ __device__ __forceinline__ uint32_t dense_tile(const T* s_in, int c0, T* outp, i
       S(a + 3, S3);
       sep::merge5(S1, S2, P1);
       sep::core4_5(Pm1, P1, c);
-      put(a, sep::final5(c, Sm2));
-      put(a + 1, sep::final5(c, S3));
+      if constexpr (FUSED) {
+        // window rows: a-2 | a-1 .. a+2 (shared) | a+3
+        const uint32_t tn = vmin2(Pm1[0], P1[0]), tx = vmax2(Pm1[9], P1[9]);
+        put_f(a, sep::final5(c, Sm2), vmin2(tn, Sm2[0]), vmax2(tx, Sm2[4]));
+        put_f(a + 1, sep::final5(c, S3), vmin2(tn, S3[0]), vmax2(tx, S3[4]));
+      } else {
+        put(a, sep::final5(c, Sm2));
+        put(a + 1, sep::final5(c, S3));
+      }
 #pragma unroll
       for (int i = 0; i < 10; ++i) Pm1[i] = P1[i];
 #pragma unroll
@@ -157,6 +194,10 @@ __device__ __forceinline__ uint32_t dense_tile(const T* s_in, int c0, T* outp, i
         S1[i] = S3[i];
       }
     }
+  }
+  if constexpr (FUSED) {
+    *detected = (uint32_t)(2 * rows) - ((sacc & 0xFFFFu) + (sacc >> 16));
+    replaced = (racc & 0xFFFFu) + (racc >> 16);
   }
   return replaced;
 }

@@ -311,6 +311,7 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
   auto dst_is_out = [&](int q) { return !MP || ((p.passes - 1 - q) & 1) == 0; };
   auto tile_at = [&](int t) { return MP ? tile_of_mp(p, t, tiles_per_frame) : tile_of(p, t, tiles_per_frame); };
   uint32_t replaced = 0, detected = 0;
+  bool pred_dense = false;  // k = 5 / 7 FNR: this warp's last tile took the dense stage
 
   // lane 0: grab a warp tile, publish it beside the stage, start its TMA load (or
   // arrive empty past the end); the mbarrier's release/acquire publishes the info.
@@ -424,7 +425,23 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
     T* const out_tile = out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.y0 - p.row_begin) * p.out_pitch + ti.x0;
     const bool ok0 = 2 * lane < valid_w, ok1 = 2 * lane + 1 < valid_w;
     int n;
-    if (fnr) {
+    bool fused = false;
+    if constexpr (kDense<K>) {
+      // the previous tile of this warp was dense: skip the detector, take the detector from
+      // the dense stage's sorted rows (whole tiles only), and re-predict from this tile
+      if (fnr && pred_dense && valid_w == WW && valid_h == ti.rows) {
+        fused = true;
+        const uint32_t none[2] = {0u, 0u};
+        uint32_t det_t = 0;
+        replaced += dense_tile<T, K, BOXW, true>(s_in, c0, out_tile + 2 * lane, p.out_pitch, ti.rows, valid_h,
+                                                 true, true, none, true, p.one, &det_t);
+        detected += det_t;
+        n = (int)__reduce_add_sync(0xffffffffu, det_t);
+        pred_dense = n * WH > p.dense_min * ti.rows;
+      }
+    }
+    if (fused) {
+    } else if (fnr) {
       uint32_t flags[2];
       T* outp = out_tile + 2 * lane;
       if (valid_w == WW && valid_h == WH) {
@@ -463,8 +480,9 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
         if (p.dense_min >= 0 && n * WH > p.dense_min * ti.rows) {  // dense_min: per full-height tile
           dense = true;
           replaced += dense_tile<T, K, BOXW>(s_in, c0, out_tile + 2 * lane, p.out_pitch, ti.rows, valid_h, ok0,
-                                             ok1, flags, true, p.one << 16);
+                                             ok1, flags, true, p.one);
         }
+        pred_dense = dense;
       }
       for (int q0 = 0; q0 < (dense ? 0 : n); q0 += QCAP) {
         if (off < q0 + QCAP && off + cnt > q0) {
@@ -489,7 +507,7 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
       const uint32_t none[2] = {0u, 0u};
       n = valid_h * valid_w;
       dense_tile<T, K, BOXW>(s_in, c0, out_tile + 2 * lane, p.out_pitch, ti.rows, valid_h, ok0, ok1, none, false,
-                             p.one << 16);
+                             p.one);
     } else {
       const int cols = max(0, valid_w), rows = max(0, valid_h);
       n = rows * cols;
