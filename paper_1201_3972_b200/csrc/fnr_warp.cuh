@@ -246,6 +246,104 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
   }
 }
 
+// Detector for large windows (k >= 11): the same per-row horizontal min / max, but the
+// vertical K-row min / max by blocks of K input rows (van Herk / Gil-Werman): within a
+// block a running prefix, at its end the suffixes, and an output row whose window ends in
+// row i of block b is min(suffix_{b-1}[i+1], prefix_b[i]) — 6 two-input ops per row for
+// min and max instead of 2 (K-1)/2 three-input ones. The block loop is rolled (one block
+// of K rows unrolled, ~8 KB of SASS for 11x11 instead of ~27 KB for the 42 unrolled rows),
+// so the detector and the 121-input median network no longer evict each other from the
+// instruction cache (c4's top stall was no_instruction).
+#ifndef IRDN_ROLLED_MIN_K
+#define IRDN_ROLLED_MIN_K 11
+#endif
+template <typename T, int K, bool FULL, int ROWS = WH>
+__device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, int64_t pitch, int valid_rows,
+                                              bool ok0, bool ok1, uint32_t (&flags)[2], uint32_t one) {
+  static_assert(ROWS <= 32, "flag streams hold 32 rows");
+  using G = Geo<T, K>;
+  constexpr int r = G::r, BOXW = G::BOXW;
+  constexpr int J = (r + 1) / 2;
+  constexpr int NIN = ROWS + 2 * r;          // box rows
+  constexpr int NB = (ROWS + K - 1) / K;     // output blocks of K rows
+  const uint32_t m1 = 0u - one, k65536 = one << 16;
+  const T* rowb = s_in + c0;
+  // horizontal K-wide min / max (and the centre word) of box row s
+  auto hrow = [&](int s, uint32_t& mn, uint32_t& mx, uint32_t& cen) {
+    const T* rowp = rowb + min(s, NIN - 1) * BOXW;  // rows past the box feed no output
+    uint32_t wd[2 * J + 1];
+#pragma unroll
+    for (int j = -J; j <= J; ++j) wd[j + J] = tile::load_pair<T>(rowp, 2 * j);
+    uint32_t ops[K];
+#pragma unroll
+    for (int d = -r; d <= r; ++d)
+      ops[d + r] = (d & 1) == 0 ? wd[J + d / 2] : shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536);
+    mn = tile::reduce_min<K>(ops);
+    mx = tile::reduce_max<K>(ops);
+    cen = wd[J];
+  };
+  // Previous block: suffix min / max from position j to K-1, and centre words, position j
+  // <-> box row 2r + (b-1)K + j. Prologue: box rows 0 .. 2r-1 at positions 1 .. K-1.
+  uint32_t hn[K], hx[K], cp[K];
+  {
+    uint32_t cn[K], cx[K];
+#pragma unroll
+    for (int j = 1; j < K; ++j) hrow(j - 1, cn[j], cx[j], cp[j]);
+    hn[K - 1] = cn[K - 1];
+    hx[K - 1] = cx[K - 1];
+#pragma unroll
+    for (int j = K - 2; j >= 1; --j) {
+      hn[j] = vmin2(cn[j], hn[j + 1]);
+      hx[j] = vmax2(cx[j], hx[j + 1]);
+    }
+    hn[0] = hx[0] = cp[0] = 0u;
+  }
+  uint32_t st0 = 0u, st1 = 0u;  // flag streams: bit y = row y of pixel 0 / pixel 1
+  T* orow = outp;
+#pragma unroll 1
+  for (int b = 0; b < NB; ++b) {
+    // block b: box rows 2r + bK + i (output row y = bK + i ends its window there)
+    uint32_t cn[K], cx[K], cc[K], gn = 0u, gx = 0u, blk = 0u;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      hrow(2 * r + b * K + i, cn[i], cx[i], cc[i]);
+      gn = i == 0 ? cn[0] : vmin2(gn, cn[i]);
+      gx = i == 0 ? cx[0] : vmax2(gx, cx[i]);
+      const uint32_t vmn = i == K - 1 ? gn : vmin2(hn[i + 1], gn);
+      const uint32_t vmx = i == K - 1 ? gx : vmax2(hx[i + 1], gx);
+      const uint32_t c = i >= r ? cc[i - r] : cp[i + K - r];  // centre: box row y + r
+      // lane of m == 0 <=> centre is the window min or max; e: bit 15 / 31 set in noisy lanes
+      const uint32_t m = vmin2(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c));
+      const uint32_t e = ~fma_add(m, one, 0x7FFF7FFFu) & 0x80008000u;
+      blk |= e >> (15 - i);  // row i of the block at bits i and 16 + i
+      if (b * K + i < ROWS) {
+        if (FULL) tile::store_pair_g<T>(orow, c, true, true);
+        else if (b * K + i < valid_rows) tile::store_pair_g<T>(orow, c, ok0, ok1);
+        orow += pitch;
+      }
+    }
+    constexpr uint32_t kBlk = (1u << K) - 1u;
+    st0 |= (blk & kBlk) << (b * K);
+    st1 |= ((blk >> 16) & kBlk) << (b * K);
+    hn[K - 1] = cn[K - 1];
+    hx[K - 1] = cx[K - 1];
+#pragma unroll
+    for (int i = K - 2; i >= 0; --i) {
+      hn[i] = vmin2(cn[i], hn[i + 1]);
+      hx[i] = vmax2(cx[i], hx[i + 1]);
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) cp[i] = cc[i];
+  }
+  if constexpr (ROWS < 32) {
+    st0 &= (1u << ROWS) - 1u;
+    st1 &= (1u << ROWS) - 1u;
+  }
+  // detect()'s layout: row y at bits y % 16 (pixel 0) and 16 + y % 16 (pixel 1) of flags[y / 16]
+  flags[0] = tile::prmt(st0, st1, 0x5410u);
+  flags[1] = tile::prmt(st0, st1, 0x7632u);
+}
+
 // Median of queued pixels (entries y << 8 | x in warp-tile coords), two per lane.
 template <typename T, int K>
 __device__ __forceinline__ uint32_t medians(const T* s_in, const uint16_t* q, int n, T* out_tile, int64_t pitch,
@@ -445,12 +543,17 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
       uint32_t flags[2];
       T* outp = out_tile + 2 * lane;
       if (valid_w == WW && valid_h == WH) {
-        detect<T, K, true>(s_in, c0, outp, p.out_pitch, WH, true, true, flags, p.one);
+        if constexpr (K >= IRDN_ROLLED_MIN_K) detect_rolled<T, K, true>(s_in, c0, outp, p.out_pitch, WH, true, true, flags, p.one);
+        else detect<T, K, true>(s_in, c0, outp, p.out_pitch, WH, true, true, flags, p.one);
       } else if (WH == 32 && valid_w == WW && valid_h == WH / 2 && ti.rows == WH / 2) {
-        detect<T, K, true, WH / 2>(s_in, c0, outp, p.out_pitch, WH / 2, true, true, flags, p.one);
+        if constexpr (K >= IRDN_ROLLED_MIN_K)
+          detect_rolled<T, K, true, WH / 2>(s_in, c0, outp, p.out_pitch, WH / 2, true, true, flags, p.one);
+        else detect<T, K, true, WH / 2>(s_in, c0, outp, p.out_pitch, WH / 2, true, true, flags, p.one);
         flags[1] = 0u;
       } else {
-        detect<T, K, false>(s_in, c0, outp, p.out_pitch, valid_h, ok0, ok1, flags, p.one);
+        if constexpr (K >= IRDN_ROLLED_MIN_K)
+          detect_rolled<T, K, false>(s_in, c0, outp, p.out_pitch, valid_h, ok0, ok1, flags, p.one);
+        else detect<T, K, false>(s_in, c0, outp, p.out_pitch, valid_h, ok0, ok1, flags, p.one);
         const uint32_t colm = (ok0 ? 0xFFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
