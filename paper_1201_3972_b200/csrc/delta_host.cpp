@@ -23,15 +23,6 @@ static inline int64_t table_bytes(int64_t n) { return ((nblocks(n) * 4) + 15) & 
 static inline int64_t mask_offset(int64_t n) { return 16 + 2 * table_bytes(n); }
 static inline int64_t values_offset(int64_t n) { return mask_offset(n) + nblocks(n) * (BLK / 8); }
 
-// streaming (non-temporal) stores for the output; IRDN_DECODE_NT=1 enables them (experiments)
-static bool use_nt() {
-  static const int v = [] {
-    const char* e = getenv("IRDN_DECODE_NT");
-    return e ? atoi(e) : 0;  // off: measured slower on the B200 box (c2 1.11 vs 1.00 ms per call)
-  }();
-  return v != 0;
-}
-
 template <typename T>
 static void block_scalar(const T* in, T* out, int64_t m, const uint32_t* mask, const T* vals, uint32_t cnt) {
   memcpy(out, in, (size_t)m * sizeof(T));
@@ -54,23 +45,13 @@ __attribute__((target("avx512f,avx512bw,avx512vbmi2"))) static void block_avx512
     return;
   }
   const int64_t full = m / 32;
-  if (use_nt() && ((uintptr_t)out & 63) == 0) {  // streaming stores: no read-for-ownership of the output lines
-    for (int64_t w = 0; w < full; ++w) {
-      const uint32_t x = mask[w];
-      __m512i v = _mm512_loadu_si512(in + 32 * w);
-      v = _mm512_mask_expandloadu_epi16(v, (__mmask32)x, vals);
-      _mm512_stream_si512(reinterpret_cast<__m512i*>(out + 32 * w), v);
-      vals += __builtin_popcount(x);
-    }
-    _mm_sfence();  // this thread's streaming stores are ordered before the team's barrier
-  } else {
-    for (int64_t w = 0; w < full; ++w) {
-      const uint32_t x = mask[w];
-      __m512i v = _mm512_loadu_si512(in + 32 * w);
-      v = _mm512_mask_expandloadu_epi16(v, (__mmask32)x, vals);
-      _mm512_storeu_si512(out + 32 * w, v);
-      vals += __builtin_popcount(x);
-    }
+  // (streaming stores were measured slower here: c2 1.11 vs 1.00 ms per call)
+  for (int64_t w = 0; w < full; ++w) {
+    const uint32_t x = mask[w];
+    __m512i v = _mm512_loadu_si512(in + 32 * w);
+    v = _mm512_mask_expandloadu_epi16(v, (__mmask32)x, vals);
+    _mm512_storeu_si512(out + 32 * w, v);
+    vals += __builtin_popcount(x);
   }
   if (m > full * 32) block_scalar<uint16_t>(in + full * 32, out + full * 32, m - full * 32, mask + full, vals, 1);
 }
@@ -82,18 +63,13 @@ __attribute__((target("avx512f,avx512bw,avx512vbmi2"))) static void block_avx512
     return;
   }
   const int64_t full = m / 64;
-  const bool nt = use_nt() && ((uintptr_t)out & 63) == 0;
   for (int64_t w = 0; w < full; ++w) {
     const uint64_t x = (uint64_t)mask[2 * w] | ((uint64_t)mask[2 * w + 1] << 32);
     __m512i v = _mm512_loadu_si512(in + 64 * w);
     v = _mm512_mask_expandloadu_epi8(v, (__mmask64)x, vals);
-    if (nt)
-      _mm512_stream_si512(reinterpret_cast<__m512i*>(out + 64 * w), v);
-    else
-      _mm512_storeu_si512(out + 64 * w, v);
+    _mm512_storeu_si512(out + 64 * w, v);
     vals += __builtin_popcountll(x);
   }
-  if (nt) _mm_sfence();
   if (m > full * 64) block_scalar<uint8_t>(in + full * 64, out + full * 64, m - full * 64, mask + 2 * full, vals, 1);
 }
 

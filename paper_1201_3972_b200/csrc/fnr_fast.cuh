@@ -198,67 +198,6 @@ inline unsigned int* sched_slot(int dev, cudaStream_t s) {
   return pool[dev] + slot * 32;
 }
 
-template <typename T, int K>
-inline int launch_tile(const T* d_in, T* d_out, const PassGeom& g, int method, unsigned long long* counts,
-                       cudaStream_t s, bool* taken) {
-  using G = tile::Geo<T, K>;
-  *taken = false;
-  CUtensorMap in_map;
-  const int out_rows = g.row_end - g.row_begin;
-  if (!make_map<T>(&in_map, d_in, g.width, g.in_rows, g.batch, g.in_pitch, g.in_frame_stride, G::BOXW, G::BOXH))
-    return 0;
-  // persistent grid: as many CTAs as fit on the device at once (cached per kernel)
-  static int blocks_per_sm = 0;
-  if (blocks_per_sm == 0) {
-    cudaFuncSetAttribute(tile::fnr_tile_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tile::fnr_tile_kernel<T, K>, tile::THREADS, G::SMEM) !=
-            cudaSuccess ||
-        n < 1) {
-      cudaGetLastError();
-      n = 1;
-    }
-    blocks_per_sm = n;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  sms = sm_count(dev);
-  unsigned int* sched = sched_slot(dev, s);
-  if (!sched) return 0;
-  tile::TileParams p;
-  p.out = d_out;
-  p.out_pitch = g.out_pitch;
-  p.out_frame = g.out_frame_stride;
-  p.width = g.width;
-  p.height = g.height;
-  p.in_row0 = g.in_row0;
-  p.row_begin = g.row_begin;
-  p.row_end = g.row_end;
-  p.tiles_x = (g.width + tile::TW - 1) / tile::TW;
-  p.tiles_y = (out_rows + tile::TH - 1) / tile::TH;
-  p.batch = g.batch;
-  p.method = method;
-  p.counts = counts;
-  p.sched = sched;
-  p.one = 1u;
-  p.dense_min = -1;
-  p.debug = getenv("IRDN_DEBUG") ? atoi(getenv("IRDN_DEBUG")) : 0;
-  p.full_tiles = 0;
-  p.static_rounds = 0;
-  p.debug_buf = nullptr;
-  const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
-  if (ntiles > 0x7fffffffLL) return 0;
-  dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));
-  *taken = true;
-  cudaError_t e = launch_pdl(tile::fnr_tile_kernel<T, K>, grid, dim3(tile::THREADS), G::SMEM, s, in_map, p);
-  if (e == cudaSuccess) e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    g_fast_err = cudaGetErrorString(e);
-    return 1;
-  }
-  return 0;
-}
-
 #ifdef IRDN_TIMELINE
 // Experiments only: per-tile (wait, ready, detected, done, n, warp << 16 | smid) of the last warp-kernel launch.
 inline unsigned long long* g_timeline = nullptr;
@@ -309,7 +248,6 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.sched = sched;
   p.one = 1u;
   p.dense_min = dense_min_for<K>();
-  p.debug = 0;
   p.debug_buf = nullptr;
 #ifdef IRDN_TIMELINE
   if (!g_timeline) cudaMalloc(&g_timeline, 8 << 20);
@@ -437,7 +375,6 @@ inline int launch_warp_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, 
   p.sched = sched;
   p.one = 1u;
   p.dense_min = dense_min_for<K>();
-  p.debug = 0;
   p.debug_buf = nullptr;
   p.passes = passes;
   p.tmp = d_tmp;
@@ -473,11 +410,10 @@ inline int launch_warp_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, 
 // frames only; false when the layout or k does not qualify (the caller then runs the
 // passes as separate launches). Opt-in (irdn_set_multipass / IRDN_MULTIPASS=1): measured
 // slower than back-to-back single-pass launches on B200.
-inline int kernel_family();
 template <typename T>
 inline bool try_launch_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, int k, int method, int passes,
                           unsigned long long* counts, cudaStream_t s, int* rc) {
-  if (passes < 2 || kernel_family() != 1) return false;
+  if (passes < 2) return false;
   const size_t bpp = sizeof(T);
   if (((uintptr_t)d_in & 15) || ((uintptr_t)d_out & 15) || ((uintptr_t)d_tmp & 15)) return false;
   if ((g.in_pitch * bpp) % 16 || (g.out_pitch * bpp) % 16) return false;
@@ -499,17 +435,6 @@ inline bool try_launch_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, 
   if (!taken) return false;
   *rc = e ? 2 : 0;
   return true;
-}
-
-// Kernel family for k = 5..11 (and k = 3 on u16): the warp-autonomous kernel; the
-// CTA-tile kernel stays selectable for comparison with IRDN_KERNEL=tile.
-inline int kernel_family() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("IRDN_KERNEL");
-    v = (e && e[0] == 't') ? 0 : 1;
-  }
-  return v;
 }
 
 template <int BAND, bool FULL, bool FNR>
@@ -610,10 +535,7 @@ inline bool try_launch(const T* d_in, T* d_out, const PassGeom& g, int k, int me
   if (g.width < 16 || g.height < 1) return false;
   bool taken = false;
   int e = 0;
-  const int fam = kernel_family();
-#define IRDN_LAUNCH_K(KK)                                                    \
-  (fam == 0 ? launch_tile<T, KK>(d_in, d_out, g, method, counts, s, &taken) \
-            : launch_warp<T, KK>(d_in, d_out, g, method, counts, s, &taken))
+#define IRDN_LAUNCH_K(KK) launch_warp<T, KK>(d_in, d_out, g, method, counts, s, &taken)
   switch (k) {
     case 3:
       if constexpr (sizeof(T) == 1) e = launch_k3(d_in, d_out, g, method, counts, s, &taken);

@@ -144,7 +144,7 @@ __device__ __forceinline__ void make_keys(const RowSeg& t, const RowSeg& b, uint
   k[COLS + 1] = tile::prmt(tile::prmt(t.r, b.r, 0x4400u), KEY_BYTE, 0x4240u);
 }
 
-// Replicate-edge fix-up of the box cells outside the frame (see tile::fix_edges).
+// Replicate-edge fix-up of the box cells outside the frame (TMA zero-fills them).
 template <int BAND>
 __device__ __forceinline__ void fix_edges(uint8_t* s_in, int gx_lo, int gy_lo, int width, int height) {
   constexpr int BOXW = Geo<BAND>::BOXW, BOXH = Geo<BAND>::BOXH, A = Geo<BAND>::R;

@@ -158,7 +158,7 @@ __device__ __forceinline__ void fix_edges_warp(T* s_in, int gx_lo, int gy_lo, in
   __syncwarp();
 }
 
-// Detector over the warp tile (tile::detect_strip with this box geometry).
+// Detector over the warp tile.
 //
 // Per input row: the K-wide horizontal min / max of the lane's column pair (2J+1 aligned
 // words, odd offsets shifted in). Vertically, output rows are produced in pairs (j, j+1)

@@ -437,25 +437,10 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
     }();
     const int64_t target = std::max<int64_t>(1, chunk_bytes / (int64_t)sizeof(T) / frame);  // ~8 MB of frames (measured optimum for c2: tools/pcie_probe.py)
     const int64_t nchunks = std::min<int64_t>(std::max<int64_t>(1, batch / target), 256);
-    static const int taper = getenv("IRDN_TAPER") ? atoi(getenv("IRDN_TAPER")) : 0;
-    if (taper && nchunks > 1) {
-      // equal chunks, then halving ones: the chunk whose result is handled last is small
-      const int64_t per = (batch + nchunks - 1) / nchunks;
-      int64_t a = 0;
-      while (batch - a > 2 * per) {
-        chunks.push_back({a, per, 0, height});
-        a += per;
-      }
-      while (a < batch) {
-        const int64_t take = std::max<int64_t>(1, (batch - a + 1) / 2);
-        chunks.push_back({a, take, 0, height});
-        a += take;
-      }
-    } else {
-      for (int64_t i = 0; i < nchunks; ++i) {
-        int64_t a = batch * i / nchunks, b = batch * (i + 1) / nchunks;
-        if (b > a) chunks.push_back({a, b - a, 0, height});
-      }
+    // (halving chunk sizes towards the end was measured neutral)
+    for (int64_t i = 0; i < nchunks; ++i) {
+      int64_t a = batch * i / nchunks, b = batch * (i + 1) / nchunks;
+      if (b > a) chunks.push_back({a, b - a, 0, height});
     }
   } else if (passes == 1 && height >= 4 * (int64_t)(r + 1) && frame * (int64_t)sizeof(T) >= (16 << 20)) {
     const int64_t nchunks = std::min<int64_t>(16, height / (4 * (r + 1)));

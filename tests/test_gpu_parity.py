@@ -312,33 +312,6 @@ def test_concurrent_calls_from_threads_and_streams(cuda_ok):
         assert np.array_equal(g, w) and gst == wst
 
 
-def test_cta_tile_kernel_family_matches_oracle(cuda_ok, tmp_path):
-    """IRDN_KERNEL=tile selects the CTA-tile kernel (csrc/fnr_tile.cuh) kept for comparison;
-    it must stay bit-exact too (run in a subprocess: the selection is read once)."""
-    import subprocess
-    import sys
-
-    script = tmp_path / "tile_check.py"
-    script.write_text(
-        "import sys, numpy as np\n"
-        f"sys.path.insert(0, {str(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))!r})\n"
-        f"sys.path.insert(0, {os.path.dirname(os.path.abspath(__file__))!r})\n"
-        "import paper_1201_3972_b200 as P\n"
-        "from oracle import oracle\n"
-        "from paper_1201_3972_b200.scene import CONFIGS, generate\n"
-        "for name, k in (('c2', 5), ('c3', 7), ('c4', 11)):\n"
-        "    cfg = CONFIGS[name].with_shape(height=300, width=400)\n"
-        "    img = generate(cfg, nframes=2)\n"
-        "    got, st = P.run_filter(img, P.WindowSpec(k), 'fnr', 1)\n"
-        "    want, wst = oracle.run_filter_c(img, k, 'fnr', 1, threads=8)\n"
-        "    assert np.array_equal(got, want), name\n"
-        "    assert [st.minmax_scans, st.sorts, st.replacements, st.detected, st.passes] == list(wst.counters())\n"
-        "print('tile ok')\n")
-    env = dict(os.environ, IRDN_KERNEL="tile")
-    out = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=600)
-    assert out.returncode == 0 and "tile ok" in out.stdout, out.stderr[-2000:]
-
-
 @pytest.mark.parametrize("in_pinned,out_pinned", [(False, False), (True, False), (False, True), (True, True)])
 def test_host_entry_pinned_and_pageable_buffers(cuda_ok, in_pinned, out_pinned):
     """irdn_run_filter_*: pinned caller buffers are DMA'd directly, pageable ones go through
