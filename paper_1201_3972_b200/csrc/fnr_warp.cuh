@@ -158,6 +158,42 @@ __device__ __forceinline__ void fix_edges_warp(T* s_in, int gx_lo, int gy_lo, in
   __syncwarp();
 }
 
+// K-wide horizontal min / max of one smem row for the lane's column pair (u16x2), and the
+// centre word. Odd r (k = 3, 7, 11): with aligned words w_j = columns (x+2j, x+2j+1),
+// pixel x needs the low halves of w_-(r-1)/2 .. w_(r-1)/2 and the high halves of
+// w_-(r+1)/2 .. w_(r-1)/2, pixel x+1 the mirror image, so one word-wise reduction M over
+// the r middle words serves both: min(x) = min(M.lo, M.hi, w_-(r+1)/2.hi) and
+// min(x+1) = min(M.hi, M.lo, w_(r+1)/2.lo), i.e. vmin3(M, swap(M), C) with one shared
+// PRMT for C — 6 VIMNMX3 + 3 PRMT for 11x11 min and max instead of 10 VIMNMX3 + 6 shifted
+// words (12 IMAD). Even r (k = 5, 9): the k words at every offset (odd ones shifted in).
+template <typename T, int K>
+__device__ __forceinline__ void row_minmax(const T* rowp, uint32_t& mn, uint32_t& mx, uint32_t& cen,
+                                           uint32_t k65536) {
+  constexpr int r = K / 2, J = (r + 1) / 2;
+  uint32_t wd[2 * J + 1];
+#pragma unroll
+  for (int j = -J; j <= J; ++j) wd[j + J] = tile::load_pair<T>(rowp, 2 * j);
+  cen = wd[J];
+  if constexpr ((r & 1) == 1) {
+    uint32_t mid[2 * J - 1];
+#pragma unroll
+    for (int i = 0; i < 2 * J - 1; ++i) mid[i] = wd[i + 1];
+    const uint32_t a = tile::reduce_min<2 * J - 1>(mid), b = tile::reduce_max<2 * J - 1>(mid);
+    const uint32_t c = tile::prmt(wd[0], wd[2 * J], 0x5432u);  // (w_-J.hi, w_J.lo)
+    mn = vmin3(a, tile::prmt(a, a, 0x1032u), c);
+    mx = vmax3(b, tile::prmt(b, b, 0x1032u), c);
+  } else {
+    uint32_t ops[K];
+#pragma unroll
+    for (int d = -r; d <= r; ++d)
+      ops[d + r] = (d & 1) == 0 ? wd[J + d / 2]
+                   : (IRDN_DET_FMA ? shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536)
+                                   : tile::prmt(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], 0x5432u));
+    mn = tile::reduce_min<K>(ops);
+    mx = tile::reduce_max<K>(ops);
+  }
+}
+
 // Detector over the warp tile.
 //
 // Per input row: the K-wide horizontal min / max of the lane's column pair (2J+1 aligned
@@ -213,18 +249,7 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
   };
 #pragma unroll
   for (int s = 0; s < ROWS + 2 * r; ++s) {
-    uint32_t wd[2 * J + 1];
-#pragma unroll
-    for (int j = -J; j <= J; ++j) wd[j + J] = tile::load_pair<T>(rowp + s * BOXW, 2 * j);
-    uint32_t ops[K];
-#pragma unroll
-    for (int d = -r; d <= r; ++d)
-      ops[d + r] = (d & 1) == 0 ? wd[J + d / 2]
-                   : (IRDN_DET_FMA ? shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536)
-                                   : tile::prmt(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], 0x5432u));
-    rmin[s % KR] = tile::reduce_min<K>(ops);
-    rmax[s % KR] = tile::reduce_max<K>(ops);
-    rcen[s % CR] = wd[J];
+    row_minmax<T, K>(rowp + s * BOXW, rmin[s % KR], rmax[s % KR], rcen[s % CR], k65536);
     if constexpr (VPAIR) {
       if (s >= 2 * r + 1 && ((s - 2 * r - 1) & 1) == 0) {
         const int y = s - 2 * r - 1;  // output rows y, y + 1 = input rows y .. y + 2r + 1 (= s)
@@ -270,17 +295,7 @@ __device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, in
   const T* rowb = s_in + c0;
   // horizontal K-wide min / max (and the centre word) of box row s
   auto hrow = [&](int s, uint32_t& mn, uint32_t& mx, uint32_t& cen) {
-    const T* rowp = rowb + min(s, NIN - 1) * BOXW;  // rows past the box feed no output
-    uint32_t wd[2 * J + 1];
-#pragma unroll
-    for (int j = -J; j <= J; ++j) wd[j + J] = tile::load_pair<T>(rowp, 2 * j);
-    uint32_t ops[K];
-#pragma unroll
-    for (int d = -r; d <= r; ++d)
-      ops[d + r] = (d & 1) == 0 ? wd[J + d / 2] : shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536);
-    mn = tile::reduce_min<K>(ops);
-    mx = tile::reduce_max<K>(ops);
-    cen = wd[J];
+    row_minmax<T, K>(rowb + min(s, NIN - 1) * BOXW, mn, mx, cen, k65536);  // rows past the box feed no output
   };
   // Previous block: suffix min / max from position j to K-1, and centre words, position j
   // <-> box row 2r + (b-1)K + j. Prologue: box rows 0 .. 2r-1 at positions 1 .. K-1.
