@@ -219,7 +219,8 @@ static int filter_strip(const T* d_in, int64_t in_row0, int64_t in_rows, T* d_ou
 template <typename T>
 static int run_device(const T* d_in, T* d_out, T* d_tmp, int64_t batch, int64_t height,
                       int64_t width, int32_t k, int32_t method, int32_t passes,
-                      unsigned long long* d_counts, void* stream) {
+                      unsigned long long* d_counts, void* stream, int64_t pitch = 0) {
+  if (pitch <= 0) pitch = width;
   if (passes < 1) return fail(IRDN_EINVAL, "passes must be >= 1, got %d", passes);  // filters.py:92-93
   if (passes > 1 && !d_tmp) return fail(IRDN_EINVAL, "passes > 1 needs a d_tmp buffer");
   if (passes > 1 && !g_force_generic && g_multipass) {
@@ -228,16 +229,16 @@ static int run_device(const T* d_in, T* d_out, T* d_tmp, int64_t batch, int64_t 
     if (rc) return rc;
     if (!d_in || !d_out) return fail(IRDN_EINVAL, "null buffer");
     if (method == IRDN_METHOD_FNR && !d_counts) return fail(IRDN_EINVAL, "FNR needs d_counts[2]");
-    const size_t bytes = (size_t)(batch * height * width) * sizeof(T);
+    const size_t bytes = (size_t)(batch * height * pitch) * sizeof(T);
     if (overlaps(d_in, bytes, d_out, bytes) || overlaps(d_in, bytes, d_tmp, bytes) ||
         overlaps(d_out, bytes, d_tmp, bytes))
       return fail(IRDN_EINVAL, "input, output and scratch buffers overlap");
     if ((rc = check_device(nullptr))) return rc;
     PassGeom g;
-    g.in_frame_stride = height * width;
-    g.out_frame_stride = height * width;
-    g.in_pitch = width;
-    g.out_pitch = width;
+    g.in_frame_stride = height * pitch;
+    g.out_frame_stride = height * pitch;
+    g.in_pitch = pitch;
+    g.out_pitch = pitch;
     g.height = (int32_t)height;
     g.width = (int32_t)width;
     g.in_row0 = 0;
@@ -255,7 +256,7 @@ static int run_device(const T* d_in, T* d_out, T* d_tmp, int64_t batch, int64_t 
   const T* src = d_in;
   for (int p = 0; p < passes; ++p) {
     T* dst = ((passes - 1 - p) % 2 == 0) ? d_out : d_tmp;
-    int rc = filter_pass<T>(src, dst, batch, height, width, width, width, k, method, d_counts, stream);
+    int rc = filter_pass<T>(src, dst, batch, height, width, pitch, pitch, k, method, d_counts, stream);
     if (rc) return rc;
     src = dst;
   }
@@ -273,6 +274,29 @@ static int run_device(const T* d_in, T* d_out, T* d_tmp, int64_t batch, int64_t 
 // its own input, delta_host.cpp), with the last chunk split between the two. The
 // counters come back last (FilterStats accounting: filters.py:121-126).
 // ---------------------------------------------------------------------------
+// Rows of row_bytes from src (pitch spitch bytes) to dst (pitch dpitch bytes): the host
+// path's padding of unaligned rows to the TMA kernels' 16-byte pitch and back. A DMA
+// engine moves 364-byte rows at ~4 GB/s (2-D cudaMemcpy, measured), this at HBM speed.
+__global__ void copy_rows_kernel(const uint8_t* __restrict__ src, int64_t spitch, uint8_t* __restrict__ dst,
+                                 int64_t dpitch, int64_t row_bytes, int64_t rows) {
+  const bool w4 = ((row_bytes | spitch | dpitch | (int64_t)(uintptr_t)src | (int64_t)(uintptr_t)dst) & 3) == 0;
+  const int64_t n = w4 ? row_bytes / 4 : row_bytes;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    if (w4) reinterpret_cast<uint32_t*>(dst + r * dpitch)[c] = reinterpret_cast<const uint32_t*>(src + r * spitch)[c];
+    else dst[r * dpitch + c] = src[r * spitch + c];
+  }
+}
+static void copy_rows(const void* src, int64_t spitch, void* dst, int64_t dpitch, int64_t row_bytes, int64_t rows,
+                      cudaStream_t st) {
+  const bool w4 = ((row_bytes | spitch | dpitch | (int64_t)(uintptr_t)src | (int64_t)(uintptr_t)dst) & 3) == 0;
+  const int64_t n = w4 ? row_bytes / 4 : row_bytes;
+  const dim3 grid((unsigned)((n + 255) / 256), (unsigned)std::min<int64_t>(rows, 16384));
+  copy_rows_kernel<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(src), spitch, static_cast<uint8_t*>(dst), dpitch,
+                                         row_bytes, rows);
+}
+
 struct DeviceWorkspace {
   std::mutex mu;
   void* buf = nullptr;  // [in | out | tmp] regions
@@ -419,11 +443,20 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
 
   DeviceWorkspace& ws = g_ws[device];
   std::lock_guard<std::mutex> lock(ws.mu);
+  // Device rows are padded to a multiple of 16 bytes (pitch dp) when the caller's are not
+  // (the reference's own 364-pixel rows): the TMA kernels need 16-byte aligned rows, and a
+  // 2-D copy pads them on the way in and strips the padding on the way out.
+  const int64_t align = 16 / (int64_t)sizeof(T);
+  const int64_t dp = (width % align == 0 || width < 16) ? width : (width + align - 1) / align * align;
+  const int64_t dframe = height * dp;
+  const size_t dbytes = (size_t)(batch * dframe) * sizeof(T);
   const int nbuf = passes > 1 ? 3 : 2;
-  if ((rc = ensure_workspace(ws, nbytes * nbuf))) return rc;
+  if ((rc = ensure_workspace(ws, dbytes * nbuf + (dp == width ? 0 : 2 * nbytes)))) return rc;
   T* d_in = (T*)ws.buf;
-  T* d_out = d_in + batch * frame;
-  T* d_tmp = passes > 1 ? d_out + batch * frame : nullptr;
+  T* d_out = d_in + batch * dframe;
+  T* d_tmp = passes > 1 ? d_out + batch * dframe : nullptr;
+  T* lin_in = d_in + nbuf * batch * dframe;  // padded rows only: contiguous landing / leaving zones
+  T* lin_out = lin_in + batch * frame;
   IRDN_CUDA(cudaMemsetAsync(ws.counts, 0, 2 * sizeof(unsigned long long), ws.s_comp));
 
   // Chunking: frames for a batch; row strips for a single frame with one pass.
@@ -465,6 +498,31 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   const bool row_mode = batch == 1 && chunks.size() > 1;
   auto chunk_off = [&](const Chunk& c) { return c.f0 * frame + c.y0 * width; };
   auto chunk_cnt = [&](const Chunk& c) { return row_mode ? (c.y1 - c.y0) * width : c.nf * frame; };
+  auto dev_off = [&](const Chunk& c) { return c.f0 * dframe + c.y0 * dp; };     // device layout (pitch dp)
+  auto chunk_rows = [&](const Chunk& c) { return row_mode ? c.y1 - c.y0 : c.nf * height; };
+  // copies between the caller's contiguous rows (host offset hoff) and the device's possibly
+  // padded rows: padded ones land contiguous in lin_in and are spread by copy_rows on the
+  // same stream (and gathered into lin_out before leaving)
+  auto h2d = [&](T* dst, const T* src, int64_t rows, int64_t hoff, cudaStream_t st) {
+    const size_t b = (size_t)(rows * width) * sizeof(T);
+    if (dp == width) return cudaMemcpyAsync(dst, src, b, cudaMemcpyHostToDevice, st);
+    cudaError_t e = cudaMemcpyAsync(lin_in + hoff, src, b, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+      copy_rows(lin_in + hoff, width * (int64_t)sizeof(T), dst, dp * (int64_t)sizeof(T), width * (int64_t)sizeof(T),
+                rows, st);
+      e = cudaGetLastError();
+    }
+    return e;
+  };
+  auto d2h = [&](T* dst, const T* src, int64_t rows, int64_t hoff, cudaStream_t st) {
+    const size_t b = (size_t)(rows * width) * sizeof(T);
+    if (dp == width) return cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToHost, st);
+    copy_rows(src, dp * (int64_t)sizeof(T), lin_out + hoff, width * (int64_t)sizeof(T), width * (int64_t)sizeof(T),
+              rows, st);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dst, lin_out + hoff, b, cudaMemcpyDeviceToHost, st);
+    return e;
+  };
   // Pageable caller buffers: DMA from / to pinned staging slots; the CPU copies chunk
   // i into a slot (parallel memcpy) while the copy engines move chunks i-1 and i-2.
   // Result return: sparse (only the pixels that differ from the input, delta.cuh; the
@@ -477,8 +535,9 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   // (and only for a pinned input: with a pageable one the host threads are busy staging it,
   // and the full copy wins — pageable c2 1.42-1.46 vs 1.46-1.59 ms, c4 4.12 vs 5.1-5.7 ms)
   const bool in_pinned = is_pinned(h_in);
-  const bool use_delta = g_host_return == 2 || (g_host_return == 0 && method == IRDN_METHOD_FNR &&
-                                                 sizeof(T) == 2 && copy_threads() >= 6 && in_pinned);
+  const bool use_delta = dp == width &&  // the region encoder reads contiguous rows
+                         (g_host_return == 2 || (g_host_return == 0 && method == IRDN_METHOD_FNR &&
+                                                 sizeof(T) == 2 && copy_threads() >= 6 && in_pinned));
   // Sparse return: the last chunk is rebuilt on the host after everything else has landed,
   // so its second half comes back by a plain D2H copy into the (pinned) caller buffer
   // instead, while the host rebuilds the first half (IRDN_SPLIT_LAST=0 disables).
@@ -576,9 +635,9 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   // H2D: each chunk's own rows (row mode: strips, in order).
   if (!staged_in) {
     for (size_t i = 0; i < chunks.size(); ++i) {
-      const int64_t off = chunk_off(chunks[i]), cnt = chunk_cnt(chunks[i]);
+      const int64_t off = chunk_off(chunks[i]);
       if (i == 0) tmark(0, ws.s_h2d);
-      IRDN_CUDA(cudaMemcpyAsync(d_in + off, h_in + off, cnt * sizeof(T), cudaMemcpyHostToDevice, ws.s_h2d));
+      IRDN_CUDA(h2d(d_in + dev_off(chunks[i]), h_in + off, chunk_rows(chunks[i]), off, ws.s_h2d));
       tmark(1 + 4 * i, ws.s_h2d);
       IRDN_CUDA(cudaEventRecord(ev_in[i], ws.s_h2d));
     }
@@ -601,7 +660,7 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
       }
       const int64_t off = chunk_off(chunks[j]), cnt = chunk_cnt(chunks[j]);
       par_copy(stage_in(j), h_in + off, (size_t)cnt * sizeof(T));
-      IRDN_CUDA(cudaMemcpyAsync(d_in + off, stage_in(j), cnt * sizeof(T), cudaMemcpyHostToDevice, ws.s_h2d));
+      IRDN_CUDA(h2d(d_in + dev_off(chunks[j]), stage_in(j), chunk_rows(chunks[j]), off, ws.s_h2d));
       IRDN_CUDA(cudaEventRecord(ev_in[j], ws.s_h2d));
     }
     return IRDN_OK;
@@ -621,18 +680,18 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
       IRDN_CUDA(cudaStreamWaitEvent(ws.s_comp, ev_in[last], 0));
       const int64_t in0 = std::max<int64_t>(0, c.y0 - r);
       const int64_t in1 = std::min<int64_t>(height, c.y1 + r);
-      rc = filter_strip<T>(d_in + in0 * width, in0, in1 - in0, d_out + c.y0 * width, c.y0, c.y1,
-                           height, width, width, width, k, method, ws.counts, ws.s_comp);
+      rc = filter_strip<T>(d_in + in0 * dp, in0, in1 - in0, d_out + c.y0 * dp, c.y0, c.y1,
+                           height, width, dp, dp, k, method, ws.counts, ws.s_comp);
       if (rc) return rc;
     } else {
       IRDN_CUDA(cudaStreamWaitEvent(ws.s_comp, ev_in[i], 0));
       tmark(2 + 4 * i, ws.s_comp);
-      const int64_t off = c.f0 * frame;
+      const int64_t off = c.f0 * dframe;
       rc = run_device<T>(d_in + off, d_out + off, d_tmp ? d_tmp + off : nullptr, c.nf, height,
-                         width, k, method, passes, ws.counts, ws.s_comp);
+                         width, k, method, passes, ws.counts, ws.s_comp, dp);
       if (rc) return rc;
     }
-    const int64_t off = chunk_off(c), cnt = chunk_cnt(c);
+    const int64_t off = chunk_off(c), cnt = chunk_cnt(c);  // host layout (delta: dp == width)
     if (use_delta && i != full_chunk) {  // encode out vs in into the device region, DMA its fixed part + budget
       const T* a = d_in + off;
       const T* o = d_out + off;
@@ -667,8 +726,7 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
       if ((rc = drain_out(i - kStageSlots))) return rc;  // the slot's previous chunk
       drained = i - kStageSlots + 1;
     }
-    IRDN_CUDA(cudaMemcpyAsync(staged_out ? stage_out(i) : h_out + off, d_out + off, cnt * sizeof(T),
-                              cudaMemcpyDeviceToHost, ws.s_d2h));
+    IRDN_CUDA(d2h(staged_out ? stage_out(i) : h_out + off, d_out + dev_off(c), chunk_rows(c), off, ws.s_d2h));
     if (staged_out) IRDN_CUDA(cudaEventRecord(ws.ev_out[i % kStageSlots], ws.s_d2h));
   }
   if (staged_out)
