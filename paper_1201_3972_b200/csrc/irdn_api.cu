@@ -698,21 +698,14 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
       const int vec = (((uintptr_t)a | (uintptr_t)o) & 15) == 0;
       uint8_t* dreg = ws.delta_d + delta_off[i];
       // the encode runs on the D2H stream, so the next chunk's filter does not queue behind it
-      static const int enc_own = getenv("IRDN_ENC_STREAM") ? atoi(getenv("IRDN_ENC_STREAM")) : 1;
-      cudaStream_t se = enc_own ? ws.s_d2h : ws.s_comp;
-      if (enc_own) {
-        IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
-        IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
-      }
-      IRDN_CUDA(cudaMemsetAsync(dreg, 0, 16, se));
-      tmark(3 + 4 * i, se);
-      delta::encode_kernel<T><<<(unsigned)delta::nblocks(cnt), delta::THREADS, 0, se>>>(a, o, cnt, dreg, vec);
+      // (measured neutral against the compute stream; kept off the filter's path)
+      IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
+      IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
+      IRDN_CUDA(cudaMemsetAsync(dreg, 0, 16, ws.s_d2h));
+      tmark(3 + 4 * i, ws.s_d2h);
+      delta::encode_kernel<T><<<(unsigned)delta::nblocks(cnt), delta::THREADS, 0, ws.s_d2h>>>(a, o, cnt, dreg, vec);
       IRDN_CUDA(cudaGetLastError());
       note_launch();
-      if (!enc_own) {
-        IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
-        IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
-      }
       const size_t bytes = (size_t)(delta::values_offset(cnt) + delta_budget(cnt) * (int64_t)sizeof(T));
       IRDN_CUDA(cudaMemcpyAsync(ws.delta_h + delta_off[i], dreg, bytes, cudaMemcpyDeviceToHost, ws.s_d2h));
       d2h_bytes += bytes;

@@ -152,16 +152,18 @@ def _run_gray(lib, img, spec: WindowSpec, m: int, passes: int, device: int):
     src = np.frombuffer(img.pixels, dtype=np.uint16 if getattr(img.pixels, "itemsize", 1) == 2 else np.uint8)
     if src.size != w * h:
         raise ValueError(f"pixel buffer has {src.size} entries, expected {w * h}")
-    out = np.empty_like(src)
-    st = _native.IrdnStats()
-    fn = lib.irdn_run_filter_u8 if src.dtype == np.uint8 else lib.irdn_run_filter_u16
-    _native.check(fn(src.ctypes.data, out.ctypes.data, 1, h, w, spec.k, m, passes, device, ctypes.byref(st)))
+    # the native call writes straight into the result's own buffer (filters.py:108: a fresh
+    # bytearray), with no intermediate copy
     if src.dtype == np.uint8:
-        pixels = bytearray(out.tobytes())
+        pixels = bytearray(w * h)
     else:
         from array import array
 
-        pixels = array("H", out.tobytes())
+        pixels = array("H", bytes(2 * w * h))
+    out = np.frombuffer(pixels, dtype=src.dtype)
+    st = _native.IrdnStats()
+    fn = lib.irdn_run_filter_u8 if src.dtype == np.uint8 else lib.irdn_run_filter_u16
+    _native.check(fn(src.ctypes.data, out.ctypes.data, 1, h, w, spec.k, m, passes, device, ctypes.byref(st)))
     cls = type(img) if not isinstance(img, GrayImage) else GrayImage
     try:
         res = cls(w, h, pixels)
