@@ -108,8 +108,17 @@ def main():
         # launches of the device-resident timed region are the long ones
         full = [t for t in ours if ours and t > 0.5 * max(ours)]
         total = sum(t for _, t in launches)
+        # ALU-pipe warp-instructions: pipe utilisation x 2 warp-instructions / clk / SM (64 lanes,
+        # profiles/pipe_probe_r02.txt) x active SM cycles
+        alu_active = f(d, "sm__inst_executed_pipe_alu.sum.pct_of_peak_sustained_active")
+        cyc = f(d, "sm__cycles_active.sum")
+        alu_wi = alu_active / 100.0 * 2.0 * cyc
         entry = {
             "tag": tag,
+            "source": f"profiles/ncu_{tag}_{cfg}.txt",
+            "instr_per_px": inst * 32 / px,
+            "alu_instr_per_px": (alu_wi * 32 / px) if alu_wi == alu_wi else None,
+            "pixels_per_launch": px,
             "kernel": d.get("Kernel Name", d.get("launch__function_name", "")),
             "ncu_duration_us": dur_us,
             "dram_bytes_per_launch": dram if dram == dram else None,
