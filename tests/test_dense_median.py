@@ -86,3 +86,34 @@ def test_dense_stage_row_strips(cuda_ok):
             out, _ = sharding.run_shard_device(src, sh, h, k, method, 1)
             parts.append(out.cpu().numpy().view(np.uint16))
         assert np.array_equal(np.concatenate(parts), want[0]), method
+
+
+@pytest.mark.parametrize("frac", ["0", "0.5", "-1"])
+def test_dense_threshold_settings_agree(cuda_ok, tmp_path, frac):
+    """IRDN_DENSE_FRAC = 0 (every FNR tile dense; the fused detector from the second tile
+    of each warp on), 0.5 (mostly queue), -1 (no dense stage at all, MF included) give the
+    oracle's bytes and counters (subprocess: the setting is read once per process)."""
+    import subprocess
+    import sys
+
+    script = tmp_path / "dense_env.py"
+    script.write_text(
+        "import os, sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "import paper_1201_3972_b200 as P\n"
+        "from oracle import oracle\n"
+        "from paper_1201_3972_b200.scene import CONFIGS, generate\n"
+        "for name, k in (('c2', 5), ('c3', 7), ('c5', 3)):\n"
+        "    cfg = CONFIGS[name].with_shape(height=200, width=320)\n"
+        "    img = generate(cfg, nframes=3)\n"
+        "    for method in ('fnr', 'mf'):\n"
+        "        for kk in (5, 7):\n"
+        "            got, st = P.run_filter(img, P.WindowSpec(kk), method, 1)\n"
+        "            want, wst = oracle.run_filter_c(img, kk, method, 1, threads=8)\n"
+        "            assert np.array_equal(got, want), (name, kk, method)\n"
+        "            assert [st.minmax_scans, st.sorts, st.replacements, st.detected, st.passes] == "
+        "list(wst.counters())\n"
+        "print('dense env ok')\n")
+    env = dict(os.environ, IRDN_DENSE_FRAC=frac)
+    out = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0 and "dense env ok" in out.stdout, out.stderr[-2000:]
