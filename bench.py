@@ -155,6 +155,9 @@ NET_INSTR_PER_PAIR = {3: 30, 5: 172, 7: 514, 9: None, 11: 1833}
 # flagged fraction exceeds DENSE_FRAC (fnr_fast.cuh dense_min_for)
 DENSE_INSTR_PER_PAIR = {5: 56.0, 7: 121.5}
 DENSE_FRAC = {5: 0.30, 7: 0.22}
+# FNR tiles predicted dense take the detector from the sorted rows (fnr_dense.cuh FUSED):
+# window min / max shared within a group, the noisy test, the signal / changed lanes
+FUSED_DET_PER_PAIR = {5: 6.0, 7: 5.5}
 
 
 def static_ops(cfg, detected_fraction: float, method: str = "fnr") -> dict:
@@ -169,10 +172,10 @@ def static_ops(cfg, detected_fraction: float, method: str = "fnr") -> dict:
     net = NET_INSTR_PER_PAIR.get(K)
     dense = DENSE_INSTR_PER_PAIR.get(K)
     if dense is not None and (method == "mf" or detected_fraction > DENSE_FRAC[K]):
-        per_pair = dense + (det if method == "fnr" else 0.0)
+        per_pair = dense + (FUSED_DET_PER_PAIR[K] if method == "fnr" else 0.0)
         return {"method": f"separable {K}x{K} median of every pixel pair from shared sorted rows "
                           f"({dense} instructions per two medians)"
-                          + (" + extremum detector" if method == "fnr" else ""),
+                          + (" + extremum detector fused from the sorted rows" if method == "fnr" else ""),
                 "minmax_instr_per_px": round(per_pair / 2, 3), "minmax_lane_ops_per_px": round(per_pair, 3),
                 "detected_fraction": round(detected_fraction, 4)}
     per_pair = det + (net or 0) * detected_fraction
