@@ -632,14 +632,19 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
     if (trace) fprintf(stderr, " decoded %.1f us (%lld px, %lld changed)\n", us(), (long long)cnt, (long long)total);
     return IRDN_OK;
   };
+  // One chunk without the sparse return (small frames: c1, the paper's 364 x 244 image):
+  // copies and kernel on ONE stream, so the call pays no cross-stream event hops.
+  const bool one_stream = chunks.size() == 1 && !use_delta;
+  cudaStream_t s_h2d = one_stream ? ws.s_comp : ws.s_h2d;
+  cudaStream_t s_d2h = one_stream ? ws.s_comp : ws.s_d2h;
   // H2D: each chunk's own rows (row mode: strips, in order).
   if (!staged_in) {
     for (size_t i = 0; i < chunks.size(); ++i) {
       const int64_t off = chunk_off(chunks[i]);
-      if (i == 0) tmark(0, ws.s_h2d);
-      IRDN_CUDA(h2d(d_in + dev_off(chunks[i]), h_in + off, chunk_rows(chunks[i]), off, ws.s_h2d));
-      tmark(1 + 4 * i, ws.s_h2d);
-      IRDN_CUDA(cudaEventRecord(ev_in[i], ws.s_h2d));
+      if (i == 0) tmark(0, s_h2d);
+      IRDN_CUDA(h2d(d_in + dev_off(chunks[i]), h_in + off, chunk_rows(chunks[i]), off, s_h2d));
+      tmark(1 + 4 * i, s_h2d);
+      IRDN_CUDA(cudaEventRecord(ev_in[i], s_h2d));
     }
   }
   size_t drained = 0, issued = 0;
@@ -660,8 +665,8 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
       }
       const int64_t off = chunk_off(chunks[j]), cnt = chunk_cnt(chunks[j]);
       par_copy(stage_in(j), h_in + off, (size_t)cnt * sizeof(T));
-      IRDN_CUDA(h2d(d_in + dev_off(chunks[j]), stage_in(j), chunk_rows(chunks[j]), off, ws.s_h2d));
-      IRDN_CUDA(cudaEventRecord(ev_in[j], ws.s_h2d));
+      IRDN_CUDA(h2d(d_in + dev_off(chunks[j]), stage_in(j), chunk_rows(chunks[j]), off, s_h2d));
+      IRDN_CUDA(cudaEventRecord(ev_in[j], s_h2d));
     }
     return IRDN_OK;
   };
@@ -700,27 +705,27 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
       // the encode runs on the D2H stream, so the next chunk's filter does not queue behind it
       // (measured neutral against the compute stream; kept off the filter's path)
       IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
-      IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
-      IRDN_CUDA(cudaMemsetAsync(dreg, 0, 16, ws.s_d2h));
-      tmark(3 + 4 * i, ws.s_d2h);
-      delta::encode_kernel<T><<<(unsigned)delta::nblocks(cnt), delta::THREADS, 0, ws.s_d2h>>>(a, o, cnt, dreg, vec);
+      IRDN_CUDA(cudaStreamWaitEvent(s_d2h, ev_done[i], 0));
+      IRDN_CUDA(cudaMemsetAsync(dreg, 0, 16, s_d2h));
+      tmark(3 + 4 * i, s_d2h);
+      delta::encode_kernel<T><<<(unsigned)delta::nblocks(cnt), delta::THREADS, 0, s_d2h>>>(a, o, cnt, dreg, vec);
       IRDN_CUDA(cudaGetLastError());
       note_launch();
       const size_t bytes = (size_t)(delta::values_offset(cnt) + delta_budget(cnt) * (int64_t)sizeof(T));
-      IRDN_CUDA(cudaMemcpyAsync(ws.delta_h + delta_off[i], dreg, bytes, cudaMemcpyDeviceToHost, ws.s_d2h));
+      IRDN_CUDA(cudaMemcpyAsync(ws.delta_h + delta_off[i], dreg, bytes, cudaMemcpyDeviceToHost, s_d2h));
       d2h_bytes += bytes;
-      tmark(4 + 4 * i, ws.s_d2h);
-      IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_d2h));
+      tmark(4 + 4 * i, s_d2h);
+      IRDN_CUDA(cudaEventRecord(ev_done[i], s_d2h));
       continue;
     }
     IRDN_CUDA(cudaEventRecord(ev_done[i], ws.s_comp));
-    IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[i], 0));
+    IRDN_CUDA(cudaStreamWaitEvent(s_d2h, ev_done[i], 0));
     if (staged_out && !staged_in && i >= (size_t)kStageSlots && drained <= i - kStageSlots) {
       if ((rc = drain_out(i - kStageSlots))) return rc;  // the slot's previous chunk
       drained = i - kStageSlots + 1;
     }
-    IRDN_CUDA(d2h(staged_out ? stage_out(i) : h_out + off, d_out + dev_off(c), chunk_rows(c), off, ws.s_d2h));
-    if (staged_out) IRDN_CUDA(cudaEventRecord(ws.ev_out[i % kStageSlots], ws.s_d2h));
+    IRDN_CUDA(d2h(staged_out ? stage_out(i) : h_out + off, d_out + dev_off(c), chunk_rows(c), off, s_d2h));
+    if (staged_out) IRDN_CUDA(cudaEventRecord(ws.ev_out[i % kStageSlots], s_d2h));
   }
   if (staged_out)
     for (size_t i = drained; i < chunks.size(); ++i)
@@ -736,9 +741,9 @@ static int run_host(const T* h_in, T* h_out, int64_t batch, int64_t height, int6
   g_xfer_h2d = nbytes;
   g_xfer_d2h = d2h_bytes;
   unsigned long long counts[2] = {0, 0};
-  IRDN_CUDA(cudaStreamWaitEvent(ws.s_d2h, ev_done[chunks.size() - 1], 0));
-  IRDN_CUDA(cudaMemcpyAsync(counts, ws.counts, sizeof(counts), cudaMemcpyDeviceToHost, ws.s_d2h));
-  IRDN_CUDA(cudaStreamSynchronize(ws.s_d2h));
+  IRDN_CUDA(cudaStreamWaitEvent(s_d2h, ev_done[chunks.size() - 1], 0));
+  IRDN_CUDA(cudaMemcpyAsync(counts, ws.counts, sizeof(counts), cudaMemcpyDeviceToHost, s_d2h));
+  IRDN_CUDA(cudaStreamSynchronize(s_d2h));
   IRDN_CUDA(cudaStreamSynchronize(ws.s_comp));
   IRDN_CUDA(cudaGetLastError());
   if (trace) {
