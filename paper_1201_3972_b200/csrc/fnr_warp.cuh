@@ -220,22 +220,18 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
   constexpr bool VPAIR = IRDN_VPAIR < 0 ? K == 7 : IRDN_VPAIR != 0;
   constexpr int KR = VPAIR ? K + 1 : K;  // ring of per-row horizontal results
   constexpr int CR = r + 2;                   // ring of centre words
-  const uint32_t m1 = 0u - one, k65536 = one << 16, k2p31 = one << 31;
+  const uint32_t m1 = 0u - one, k65536 = one << 16, ones = one * 0x00010001u;
   uint32_t rmin[KR], rmax[KR], rcen[CR];
-  flags[0] = flags[1] = 0u;
   const T* rowp = s_in + c0;
   constexpr bool ROWADDR = IRDN_ROWADDR < 0 ? K <= 5 : IRDN_ROWADDR != 0;
   const uint32_t pitch_b = (uint32_t)(pitch * (int64_t)sizeof(T));  // < 2^32: rows of at most 2^31 pixels
   // flag test and signal-pixel store of output row y (window min vmn, max vmx, centre c)
+  uint32_t sig[2] = {0u, 0u};  // signal (not noisy) bits: row y at bits y % 16 and 16 + y % 16 of sig[y / 16]
   auto emit = [&](int y, uint32_t vmn, uint32_t vmx, uint32_t c) {
-    // lane of m == 0 <=> centre is the window min or max (no borrow: vmn <= c <= vmx)
-    const uint32_t m = IRDN_DET_FMA ? vmin2(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c)) : vmin2(c - vmn, vmx - c);
-    // m <= 0x7FFF per lane, so +0x7FFF sets bit 15 iff m != 0
-    const uint32_t e = IRDN_DET_FMA ? fma_add(m, one, 0x7FFF7FFFu) : m + 0x7FFF7FFFu;
-    uint32_t sh;
-    if (IRDN_DET_FMA) asm("mul.hi.u32 %0, %1, %2;" : "=r"(sh) : "r"(flags[y >> 4]), "r"(k2p31));
-    else sh = flags[y >> 4] >> 1;
-    flags[y >> 4] = (sh & 0x7FFF7FFFu) | (~e & 0x80008000u);  // row i ends at bits i / 16 + i
+    // z = min(c - vmn, vmx - c, 1) per lane: 0 <=> centre is the window min or max (no
+    // borrow: vmn <= c <= vmx), 1 otherwise; shifted into the row's bit position
+    const uint32_t z = vmin3(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c), ones);
+    sig[y >> 4] += z << (y & 15);
     if constexpr (ROWADDR) {
       // row address = base + y * pitch (one wide multiply-add per row, y is a constant)
       T* const rp = reinterpret_cast<T*>(reinterpret_cast<char*>(outp) + (uint64_t)(uint32_t)y * pitch_b);
@@ -269,6 +265,8 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
       emit(y, tile::reduce_min<KR>(rmin), tile::reduce_max<KR>(rmax), rcen[(s - r) % CR]);
     }
   }
+  flags[0] = ~sig[0];
+  flags[1] = ROWS > 16 ? ~sig[1] : 0u;
 }
 
 // Detector for large windows (k >= 11): the same per-row horizontal min / max, but the
@@ -291,7 +289,7 @@ __device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, in
   constexpr int J = (r + 1) / 2;
   constexpr int NIN = ROWS + 2 * r;          // box rows
   constexpr int NB = (ROWS + K - 1) / K;     // output blocks of K rows
-  const uint32_t m1 = 0u - one, k65536 = one << 16;
+  const uint32_t m1 = 0u - one, k65536 = one << 16, ones = one * 0x00010001u;
   const T* rowb = s_in + c0;
   // horizontal K-wide min / max (and the centre word) of box row s
   auto hrow = [&](int s, uint32_t& mn, uint32_t& mx, uint32_t& cen) {
@@ -313,7 +311,7 @@ __device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, in
     }
     hn[0] = hx[0] = cp[0] = 0u;
   }
-  uint32_t st0 = 0u, st1 = 0u;  // flag streams: bit y = row y of pixel 0 / pixel 1
+  uint32_t st0 = 0u, st1 = 0u;  // signal streams: bit y = row y of pixel 0 / pixel 1 is not noisy
   T* orow = outp;
 #pragma unroll 1
   for (int b = 0; b < NB; ++b) {
@@ -327,10 +325,8 @@ __device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, in
       const uint32_t vmn = i == K - 1 ? gn : vmin2(hn[i + 1], gn);
       const uint32_t vmx = i == K - 1 ? gx : vmax2(hx[i + 1], gx);
       const uint32_t c = i >= r ? cc[i - r] : cp[i + K - r];  // centre: box row y + r
-      // lane of m == 0 <=> centre is the window min or max; e: bit 15 / 31 set in noisy lanes
-      const uint32_t m = vmin2(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c));
-      const uint32_t e = ~fma_add(m, one, 0x7FFF7FFFu) & 0x80008000u;
-      blk |= e >> (15 - i);  // row i of the block at bits i and 16 + i
+      // z = min(c - min, max - c, 1): 0 in noisy lanes; row i of the block at bits i, 16 + i
+      blk += vmin3(fma_sub(c, m1, vmn), fma_sub(vmx, m1, c), ones) << i;
       if (b * K + i < ROWS) {
         if (FULL) tile::store_pair_g<T>(orow, c, true, true);
         else if (b * K + i < valid_rows) tile::store_pair_g<T>(orow, c, ok0, ok1);
@@ -350,10 +346,9 @@ __device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, in
 #pragma unroll
     for (int i = 0; i < K; ++i) cp[i] = cc[i];
   }
-  if constexpr (ROWS < 32) {
-    st0 &= (1u << ROWS) - 1u;
-    st1 &= (1u << ROWS) - 1u;
-  }
+  constexpr uint32_t kRows = ROWS >= 32 ? 0xFFFFFFFFu : (1u << ROWS) - 1u;
+  st0 = ~st0 & kRows;  // noisy streams
+  st1 = ~st1 & kRows;
   // detect()'s layout: row y at bits y % 16 (pixel 0) and 16 + y % 16 (pixel 1) of flags[y / 16]
   flags[0] = tile::prmt(st0, st1, 0x5410u);
   flags[1] = tile::prmt(st0, st1, 0x7632u);
