@@ -248,6 +248,8 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.sched = sched;
   p.one = 1u;
   p.dense_min = dense_min_for<K>();
+  p.tpf_magic = tile::udiv_magic((uint32_t)(p.tiles_x * p.tiles_y));
+  p.tx_magic = tile::udiv_magic((uint32_t)p.tiles_x);
   p.debug_buf = nullptr;
 #ifdef IRDN_TIMELINE
   if (!g_timeline) cudaMalloc(&g_timeline, 8 << 20);
@@ -375,6 +377,8 @@ inline int launch_warp_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, 
   p.sched = sched;
   p.one = 1u;
   p.dense_min = dense_min_for<K>();
+  p.tpf_magic = tile::udiv_magic((uint32_t)(p.tiles_x * p.tiles_y));
+  p.tx_magic = tile::udiv_magic((uint32_t)p.tiles_x);
   p.debug_buf = nullptr;
   p.passes = passes;
   p.tmp = d_tmp;

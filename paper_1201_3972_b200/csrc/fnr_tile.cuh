@@ -41,7 +41,13 @@ struct TileParams {
   // warp kernel, k = 5 / 7 (fnr_dense.cuh): FNR tiles with more than dense_min flagged
   // pixels take the dense median stage; dense_min < 0 keeps MF on the queue path too
   int32_t dense_min;
+  // warp kernel: ceil(2^32 / d) for d = tiles per frame and tiles_x (wk::udiv)
+  uint32_t tpf_magic, tx_magic;
 };
+
+inline uint32_t udiv_magic(uint32_t d) {
+  return d <= 1u ? 0xFFFFFFFFu : (uint32_t)((((uint64_t)1 << 32) + d - 1) / d);
+}
 
 struct TileInfo {
   int t, b, tx0, ty0;
