@@ -394,11 +394,12 @@ __device__ __forceinline__ uint32_t medians(const T* s_in, const uint16_t* q, in
 #pragma unroll
       for (int dx = 0; dx < K; ++dx)
         v[dy * K + dx] = (uint32_t)a[dy * BOXW + dx] | ((uint32_t)bb[dy * BOXW + dx] << 16);
+    const uint32_t cen = v[(K * K) / 2];  // both centres, packed (the network may reuse v)
     const uint32_t med = tile::median_dispatch<K * K>(v, m1);
     const uint32_t med0 = med & 0xFFFFu, med1 = med >> 16;
     out_tile[y0 * pitch + x0] = (T)med0;
     if (two) out_tile[y1 * pitch + x1] = (T)med1;
-    if (fnr) replaced += (med0 != (uint32_t)a[r * BOXW + r]) + (two && med1 != (uint32_t)bb[r * BOXW + r]);
+    if (fnr) replaced += (med0 != (cen & 0xFFFFu)) + (two && med1 != (cen >> 16));
   }
   return replaced;
 }
@@ -617,7 +618,7 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
             while (f) {
               const int bit = __ffs(f) - 1;
               f &= f - 1u;
-              if ((unsigned)idx < (unsigned)QCAP)
+              if (QCAP >= WW * WH || (unsigned)idx < (unsigned)QCAP)
                 s_q[idx] = (uint16_t)(ebase + ((uint32_t)(16 * h + (bit & 15)) << 8) + (uint32_t)(bit >> 4));
               ++idx;
             }
