@@ -484,6 +484,8 @@ inline int launch_k3_kern(const uint8_t* d_in, uint8_t* d_out, const PassGeom& g
   p.sched = sched;
   p.one = 1u;
   p.dense_min = -1;
+  p.tpf_magic = tile::udiv_magic((uint32_t)(p.tiles_x * p.tiles_y));
+  p.tx_magic = tile::udiv_magic((uint32_t)p.tiles_x);
   const long long ntiles = (long long)p.tiles_x * p.tiles_y * g.batch;
   if (ntiles > 0x7fffffffLL) return 0;
   dim3 grid((unsigned)std::min<long long>(ntiles, (long long)sms * blocks_per_sm));

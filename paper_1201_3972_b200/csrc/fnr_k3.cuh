@@ -203,13 +203,15 @@ __global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__
   uint32_t det_total = 0, rep_total = 0;
   const uint32_t one = p.one, m1 = 0u - p.one, k65536 = p.one << 16;  // opaque: keeps IMADs on the FMA pipe
 
+  // (claiming the next tile's index when a tile starts, to overlap the atomic's round trip,
+  // measured 0.5 % slower on c5: 0.7839 vs 0.7831 ms)
   auto refill = [&](int stage) {
     tile::TileInfo ti;
     ti.t = (int)atomicAdd(p.sched, 1u);
     if (ti.t < ntiles) {
-      ti.b = ti.t / tiles_per_frame;
+      ti.b = tile::udiv(ti.t, tiles_per_frame, p.tpf_magic);
       const int tt = ti.t - ti.b * tiles_per_frame;
-      const int ty = tt / p.tiles_x;
+      const int ty = tile::udiv(tt, p.tiles_x, p.tx_magic);
       ti.tx0 = (tt - ty * p.tiles_x) * TW;
       ti.ty0 = p.row_begin + ty * G::TH;
       s_tile[stage] = ti;

@@ -49,6 +49,17 @@ inline uint32_t udiv_magic(uint32_t d) {
   return d <= 1u ? 0xFFFFFFFFu : (uint32_t)((((uint64_t)1 << 32) + d - 1) / d);
 }
 
+// n / d for 0 <= n < 2^31, 1 <= d < 2^31, with the launch-invariant magic = ceil(2^32 / d)
+// (0xFFFFFFFF for d = 1): the multiply-high estimate is off by at most one either way and
+// one remainder check fixes it — a few instructions instead of the integer-division
+// sequence, in the path from the tile scheduler's atomic to the tile's TMA issue.
+__device__ __forceinline__ int udiv(int n, int d, uint32_t magic) {
+  int q = (int)__umulhi((uint32_t)n, magic);
+  const int rem = n - q * d;
+  q += rem < 0 ? -1 : (rem >= d ? 1 : 0);
+  return q;
+}
+
 struct TileInfo {
   int t, b, tx0, ty0;
 };

@@ -71,17 +71,6 @@ struct WTile {
   int t, b, x0, y0, rows, pass;
 };
 
-// n / d for 0 <= n < 2^31, 1 <= d < 2^31, with the launch-invariant magic = ceil(2^32 / d)
-// (0xFFFFFFFF for d = 1): the multiply-high estimate is off by at most one either way and
-// one remainder check fixes it — a few instructions instead of the integer-division
-// sequence, in lane 0's path from the scheduler atomic to the tile's TMA issue.
-__device__ __forceinline__ int udiv(int n, int d, uint32_t magic) {
-  int q = (int)__umulhi((uint32_t)n, magic);
-  const int rem = n - q * d;
-  q += rem < 0 ? -1 : (rem >= d ? 1 : 0);
-  return q;
-}
-
 // Tile t of the pass. The pool ends in half-height tiles (the halves of the last
 // ntiles - full_tiles full tiles, p.full_tiles.. onwards), so the warps that finish
 // last finish a short tile: with ~3.5 tiles per warp the tail of a 64 x 32 pool is
@@ -96,9 +85,9 @@ __device__ __forceinline__ WTile tile_of(const tile::TileParams& p, int t, int t
     rows = WH / 2;
     dy = (h & 1) * (WH / 2);
   }
-  ti.b = udiv(f, tiles_per_frame, p.tpf_magic);
+  ti.b = tile::udiv(f, tiles_per_frame, p.tpf_magic);
   const int tt = f - ti.b * tiles_per_frame;
-  const int ty = udiv(tt, p.tiles_x, p.tx_magic);
+  const int ty = tile::udiv(tt, p.tiles_x, p.tx_magic);
   ti.x0 = (tt - ty * p.tiles_x) * WW;
   ti.y0 = p.row_begin + ty * WH + dy;
   ti.rows = rows;
