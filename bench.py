@@ -154,7 +154,7 @@ NET_INSTR_PER_PAIR = {3: 30, 5: 172, 7: 514, 9: None, 11: 1833}
 # pair (tools/netgen/sepgen.py prints them), taken by MF always and by FNR tiles whose
 # flagged fraction exceeds DENSE_FRAC (fnr_fast.cuh dense_min_for)
 DENSE_INSTR_PER_PAIR = {5: 56.0, 7: 121.5}
-DENSE_FRAC = {5: 0.30, 7: 0.22}
+DENSE_FRAC = {5: 0.20, 7: 0.18}
 # FNR tiles predicted dense take the detector from the sorted rows (fnr_dense.cuh FUSED):
 # window min / max shared within a group, the noisy test, the signal / changed lanes
 FUSED_DET_PER_PAIR = {5: 6.0, 7: 5.5}

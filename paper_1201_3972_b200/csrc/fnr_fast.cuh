@@ -166,7 +166,9 @@ template <int K>
 inline int dense_min_for() {
   if (K != 5 && K != 7) return -1;
   static const double env = getenv("IRDN_DENSE_FRAC") ? atof(getenv("IRDN_DENSE_FRAC")) : -2.0;
-  const double frac = env > -2.0 ? env : (K == 7 ? 0.22 : 0.30);
+  // measured crossovers (tools/dense_threshold_probe.py, profiles/r02/dense_threshold_probe.jsonl:
+  // 64 x 640x512 frames, salt-and-pepper density swept): 5x5 ~20 % flagged, 7x7 ~18 %
+  const double frac = env > -2.0 ? env : (K == 7 ? 0.18 : 0.20);
   if (frac < 0.0) return -1;
   return (int)(frac * wk::WW * wk::WH);
 }
