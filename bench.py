@@ -597,6 +597,8 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
     gather = None
     if world > 1:
         gather = time_gather(outs[0], dev, rank, world, share, cfg)
+        if passes == 1:
+            gather["fused"] = time_fused_gather(ins[0], dev, rank, world, share, cfg, lib, _native, M, counts, sptr)
 
     # the dominant kernel: this rank's per-launch average over the timed region; isolated
     # per-launch events (which defeat the programmatic-dependent-launch overlap) beside it
@@ -722,6 +724,65 @@ def time_gather(out, dev, rank: int, world: int, share: dict, cfg):
     return {"ms": round(secs * 1e3, 3), "bytes": bytes_in, "backend": _BACKEND,
             "note": "outputs stay sharded during the filter; this is one gather to rank 0, "
                     "not included in value"}
+
+
+def time_fused_gather(src, dev, rank: int, world: int, share: dict, cfg, lib, _native, M, counts, sptr):
+    """The gather fused into the filter: rank 0's full output is mapped into every rank
+    (CUDA IPC, irdn_ipc_*) and each rank's filter launch stores its shard straight into it
+    (NVLink peer stores tile by tile). Timed from a common barrier to the last rank's
+    completion (host clock around a synchronised launch, max over ranks); compare with
+    value's filter-only time plus `gather.ms`."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    H, W, bpp = cfg.height, cfg.width, cfg.bytes_per_pixel
+    full = torch.empty((cfg.frames if cfg.frames > 1 else 1, H, W), dtype=src.dtype, device=dev) if rank == 0 else None
+    msg = [None]
+    if rank == 0:
+        handle, off = ctypes.create_string_buffer(64), ctypes.c_uint64(0)
+        _native.check(lib.irdn_ipc_export(full.data_ptr(), handle, ctypes.byref(off)))
+        msg = [(handle.raw, int(off.value))]
+    dist.broadcast_object_list(msg, src=0)
+    raw, off = msg[0]
+    if rank == 0:
+        base = full.data_ptr()
+    else:
+        ptr = ctypes.c_void_p()
+        _native.check(lib.irdn_ipc_open(ctypes.create_string_buffer(raw, 64), off, ctypes.byref(ptr)))
+        base = ptr.value
+    t = "u8" if bpp == 1 else "u16"
+    try:
+        def launch():
+            if share["kind"] == "rows":
+                fn = getattr(lib, f"irdn_filter_strip_{t}")
+                dst = base + share["y0"] * W * bpp
+                _native.check(fn(src.data_ptr(), share["in0"], share["in1"] - share["in0"], dst, share["y0"],
+                                 share["y1"], H, W, W, W, cfg.k, M, counts.data_ptr(), sptr))
+            else:
+                nfr = share["f1"] - share["f0"]
+                if share.get("replica"):
+                    dst = base  # replicas (c1): every rank writes the same frame
+                else:
+                    dst = base + share["f0"] * H * W * bpp
+                fn = getattr(lib, f"irdn_filter_pass_{t}")
+                _native.check(fn(src.data_ptr(), dst, nfr, H, W, W, W, cfg.k, M, counts.data_ptr(), sptr))
+        for _ in range(2):
+            launch()
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        t0 = time.perf_counter()
+        launch()
+        torch.cuda.synchronize(dev)
+        secs = _max_over_ranks(time.perf_counter() - t0, dev)
+        dist.barrier()
+    finally:
+        if rank != 0:
+            lib.irdn_ipc_close(ctypes.c_void_p(base), off)
+    return {"ms": round(secs * 1e3, 3),
+            "note": "filter launch with every rank storing its shard into rank 0's output "
+                    "(CUDA IPC mapping, NVLink peer stores); host clock, max over ranks"}
 
 
 def run_e2e(args, cfg, lib, _native, h_in, d_out_ref, share, steps, dev, world, passes, local):

@@ -211,6 +211,21 @@ IRDN_API uint64_t irdn_delta_decode_u8(const void* region, const uint8_t* h_in, 
 IRDN_API uint64_t irdn_delta_decode_u16(const void* region, const uint16_t* h_in, uint16_t* h_out, int64_t n,
                                         int32_t simd);
 
+/*
+ * Fused gather for multi-GPU shards (reference filters.py:110-126: the row bands' results
+ * land in ONE output buffer). The rank that owns the full output exports it with
+ * irdn_ipc_export (a 64-byte CUDA IPC handle of the allocation containing d_ptr, plus
+ * d_ptr's byte offset in it, so pointers from caching allocators work); every other rank
+ * maps it with irdn_ipc_open and passes (mapped pointer + its shard's offset) as d_out of
+ * irdn_run_filter_device_* / irdn_filter_strip_*: the filter kernels then store their
+ * output straight into the owner's memory over NVLink (peer stores from the same kernel,
+ * no separate gather collective). irdn_ipc_close unmaps. Works between processes on the
+ * same GPU too (the CPU test of the path).
+ */
+IRDN_API int irdn_ipc_export(const void* d_ptr, void* handle64, uint64_t* offset);
+IRDN_API int irdn_ipc_open(const void* handle64, uint64_t offset, void** d_ptr);
+IRDN_API int irdn_ipc_close(void* d_ptr, uint64_t offset);
+
 /* Kernel launches issued by this thread since the last reset (for bench accounting). */
 IRDN_API uint64_t irdn_launch_count(void);
 IRDN_API void irdn_reset_launch_count(void);

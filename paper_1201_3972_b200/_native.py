@@ -50,6 +50,7 @@ EXPORTED = [
     "irdn_set_force_generic", "irdn_inject_impulse_u8", "irdn_sq_err_sum_u8", "irdn_sq_err_sum_u16",
     "irdn_set_host_return", "irdn_last_transfer", "irdn_delta_region_bytes", "irdn_delta_encode_u8",
     "irdn_delta_encode_u16", "irdn_delta_decode_u8", "irdn_delta_decode_u16", "irdn_set_multipass",
+    "irdn_ipc_export", "irdn_ipc_open", "irdn_ipc_close",
 ]
 
 HOST_RETURN = {"auto": 0, "full": 1, "delta": 2}
@@ -98,6 +99,12 @@ def _declare(l: ctypes.CDLL) -> None:
     l.irdn_set_host_return.argtypes = [i32]
     l.irdn_last_transfer.restype = None
     l.irdn_last_transfer.argtypes = [ctypes.POINTER(u64), ctypes.POINTER(u64)]
+    l.irdn_ipc_export.restype = ctypes.c_int
+    l.irdn_ipc_export.argtypes = [vp, vp, ctypes.POINTER(u64)]
+    l.irdn_ipc_open.restype = ctypes.c_int
+    l.irdn_ipc_open.argtypes = [vp, u64, ctypes.POINTER(vp)]
+    l.irdn_ipc_close.restype = ctypes.c_int
+    l.irdn_ipc_close.argtypes = [vp, u64]
     l.irdn_delta_region_bytes.restype = u64
     l.irdn_delta_region_bytes.argtypes = [i64, i32]
     for t in ("u8", "u16"):

@@ -1011,6 +1011,55 @@ int32_t irdn_set_force_generic(int32_t on) {
   return prev;
 }
 
+// ---- fused gather: CUDA IPC of the owner's output allocation ----------------------------
+typedef CUresult (*MemGetAddressRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+static MemGetAddressRangeFn address_range_fn() {
+  static MemGetAddressRangeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<MemGetAddressRangeFn>(p);
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
+
+int irdn_ipc_export(const void* d_ptr, void* handle64, uint64_t* offset) {
+  if (!d_ptr || !handle64 || !offset) return fail(IRDN_EINVAL, "null argument");
+  MemGetAddressRangeFn range = address_range_fn();
+  if (!range) return fail(IRDN_ECUDA, "cuMemGetAddressRange is not available");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)(uintptr_t)d_ptr) != CUDA_SUCCESS)
+    return fail(IRDN_EINVAL, "pointer is not in a device allocation");
+  cudaIpcMemHandle_t h;
+  IRDN_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>((uintptr_t)base)));
+  static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+  memcpy(handle64, &h, sizeof(h));
+  *offset = (uint64_t)((uintptr_t)d_ptr - (uintptr_t)base);
+  return IRDN_OK;
+}
+
+int irdn_ipc_open(const void* handle64, uint64_t offset, void** d_ptr) {
+  if (!handle64 || !d_ptr) return fail(IRDN_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  void* base = nullptr;
+  IRDN_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *d_ptr = static_cast<char*>(base) + offset;
+  return IRDN_OK;
+}
+
+int irdn_ipc_close(void* d_ptr, uint64_t offset) {
+  if (!d_ptr) return fail(IRDN_EINVAL, "null argument");
+  IRDN_CUDA(cudaIpcCloseMemHandle(static_cast<char*>(d_ptr) - offset));
+  return IRDN_OK;
+}
+
 #ifdef IRDN_TIMELINE
 IRDN_API int irdn_debug_timeline(void* host, int64_t bytes) {
   if (!irdn::fast::g_timeline) return IRDN_EINVAL;

@@ -157,10 +157,14 @@ def run_shard(img: np.ndarray, shard: Shard, k: int, method: str, passes: int,
 # ---------------------------------------------------------------------------
 # Device executor (the product path: libirdn.so, one call per shard / strip call)
 # ---------------------------------------------------------------------------
-def run_shard_device(src, shard: Shard, height: int, k: int, method: str, passes: int, stream=None):
+def run_shard_device(src, shard: Shard, height: int, k: int, method: str, passes: int, stream=None,
+                     dst_ptr: int | None = None):
     """Filter a device-resident shard. `src` is a CUDA tensor of the shard's frames
     [f1-f0, H, W] or its input rows [in1-in0, W] (uint8, or uint16 / int16 bit patterns).
-    Returns (device output, counters); the output stays on the device."""
+    Returns (device output, counters); the output stays on the device. With `dst_ptr` (a
+    device pointer, possibly another GPU's memory mapped through CUDA IPC: the fused
+    gather) the shard's final output is written there instead and the returned tensor is
+    None."""
     import torch
 
     from . import _native
@@ -176,27 +180,37 @@ def run_shard_device(src, shard: Shard, height: int, k: int, method: str, passes
     with torch.cuda.device(dev):
         if shard.kind == "frames":
             nfr = shard.f1 - shard.f0
-            out = torch.empty((nfr, height, width), dtype=src.dtype, device=dev)
+            out = torch.empty((nfr, height, width), dtype=src.dtype, device=dev) if dst_ptr is None else None
             if nfr:
-                tmp = torch.empty_like(out) if passes > 1 else None
+                tmp = torch.empty((nfr, height, width), dtype=src.dtype, device=dev) if passes > 1 else None
                 fn = getattr(lib, f"irdn_run_filter_device_{t}")
-                _native.check(fn(src.data_ptr(), out.data_ptr(), tmp.data_ptr() if tmp is not None else None, nfr,
+                _native.check(fn(src.data_ptr(), out.data_ptr() if out is not None else dst_ptr,
+                                 tmp.data_ptr() if tmp is not None else None, nfr,
                                  height, width, k, m, passes, counts.data_ptr(), s.cuda_stream))
         else:
             fn = getattr(lib, f"irdn_filter_strip_{t}")
             junk = torch.zeros(2, dtype=torch.int64, device=dev)
             cur, cur0 = src, shard.in0
             out = torch.empty((0, width), dtype=src.dtype, device=dev)
-            for a, b, calls in strip_pass_plan(shard, height, k, passes):
-                out = torch.empty((b - a, width), dtype=src.dtype, device=dev)
+            plan = strip_pass_plan(shard, height, k, passes)
+            for pi, (a, b, calls) in enumerate(plan):
+                last = pi == len(plan) - 1
+                out = torch.empty((b - a, width), dtype=src.dtype, device=dev) if not (last and dst_ptr) else None
                 for c in calls:
-                    dst = out[c.row_begin - a:]
-                    _native.check(fn(cur[c.need0 - cur0:].data_ptr(), c.need0, c.need1 - c.need0, dst.data_ptr(),
+                    if out is not None:
+                        dst = out[c.row_begin - a:].data_ptr()
+                    else:  # the last pass produces exactly the owned rows [y0, y1)
+                        dst = dst_ptr + (c.row_begin - shard.y0) * width * src.element_size()
+                    _native.check(fn(cur[c.need0 - cur0:].data_ptr(), c.need0, c.need1 - c.need0, dst,
                                      c.row_begin, c.row_end, height, width, width, width, k, m,
                                      (counts if c.counted else junk).data_ptr(), s.cuda_stream))
                 cur, cur0 = out, a
         det, rep = (int(v) for v in counts.tolist())  # the one host sync of the shard
-    return out, _counters(method, out.numel(), passes, det, rep)
+    if shard.kind == "frames":
+        npx = (shard.f1 - shard.f0) * height * width
+    else:
+        npx = max(0, shard.y1 - shard.y0) * width
+    return out, _counters(method, npx, passes, det, rep)
 
 
 def _gather_to_rank0(local, world: int, rank: int, group, backend: str):
@@ -223,15 +237,18 @@ def _gather_to_rank0(local, world: int, rank: int, group, backend: str):
 
 
 def run_filter_distributed(img, k: int, method: str = "fnr", passes: int = 1, *,
-                           group=None, gather: bool = True, strip_fn: StripFn | None = None):
+                           group=None, gather: bool | str = True, strip_fn: StripFn | None = None):
     """run_filter over all ranks of `group` (torch.distributed, NCCL or gloo).
 
     `img` is a numpy array ([H,W] or [B,H,W], uint8 / uint16; every rank passes the same
     array, or at least its own shard's frames / rows) or a CUDA tensor of that shape.
     Returns (output, FilterStats-like dict). With gather=True rank 0 receives the full
     result (same kind as the input: numpy or tensor) and the other ranks None; otherwise
-    every rank keeps its shard (on its GPU). `strip_fn` swaps the device executor for
-    the host one (CPU tests of the decomposition).
+    every rank keeps its shard (on its GPU). gather="fused": rank 0's output buffer is
+    mapped into every rank (CUDA IPC, irdn_ipc_*) and each rank's filter kernels store their
+    shard's output straight into it over NVLink — the gather happens inside the filter
+    launch, tile by tile, instead of as a collective afterwards. `strip_fn` swaps the
+    device executor for the host one (CPU tests of the decomposition).
     """
     import torch
     import torch.distributed as dist
@@ -265,6 +282,9 @@ def run_filter_distributed(img, k: int, method: str = "fnr", passes: int = 1, *,
         else:
             a = np.ascontiguousarray(part)
             src = torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).to(dev)
+        if gather == "fused":
+            return _run_fused_gather(src, shard, shape3, ndim, k, method, passes, rank, world, group, backend,
+                                     is_tensor, orig, img)
         local_t, c = run_shard_device(src, shard, height, k, method, passes)
     tot = torch.tensor(c, dtype=torch.int64, device=local_t.device if backend == "nccl" else "cpu")
     allc = [torch.empty_like(tot) for _ in range(world)]
@@ -284,3 +304,57 @@ def run_filter_distributed(img, k: int, method: str = "fnr", passes: int = 1, *,
         return full.to(orig.device).view(orig.dtype), stats
     a = full.cpu().numpy()
     return (a.view(np.uint16) if u16 else a), stats
+
+
+def _run_fused_gather(src, shard: Shard, shape3, ndim: int, k: int, method: str, passes: int, rank: int,
+                      world: int, group, backend: str, is_tensor: bool, orig, img):
+    """The filter writes every rank's shard straight into rank 0's output (CUDA IPC)."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _native
+
+    lib = _native.load_lib()
+    batch, height, width = shape3
+    dev = src.device
+    bpp = src.element_size()
+    full = torch.empty(shape3, dtype=src.dtype, device=dev) if rank == 0 else None
+    msg = [None]
+    if rank == 0:
+        handle = ctypes.create_string_buffer(64)
+        off = ctypes.c_uint64(0)
+        _native.check(lib.irdn_ipc_export(full.data_ptr(), handle, ctypes.byref(off)))
+        msg = [(handle.raw, int(off.value))]
+    dist.broadcast_object_list(msg, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    raw, off = msg[0]
+    if rank == 0:
+        base = full.data_ptr()
+    else:
+        ptr = ctypes.c_void_p()
+        _native.check(lib.irdn_ipc_open(ctypes.create_string_buffer(raw, 64), off, ctypes.byref(ptr)))
+        base = ptr.value
+    try:
+        if shard.kind == "frames":
+            dst = base + shard.f0 * height * width * bpp
+        else:
+            dst = base + shard.y0 * width * bpp
+        _, c = run_shard_device(src, shard, height, k, method, passes, dst_ptr=dst)
+        torch.cuda.synchronize(dev)  # this rank's stores into rank 0's memory are complete
+        dist.barrier(group=group)
+    finally:
+        if rank != 0:
+            lib.irdn_ipc_close(ctypes.c_void_p(base), off)
+    tot = torch.tensor(c, dtype=torch.int64, device=dev if backend == "nccl" else "cpu")
+    allc = [torch.empty_like(tot) for _ in range(world)]
+    dist.all_gather(allc, tot, group=group)
+    scans, sorts, rep, det = (int(v) for v in torch.stack(allc).cpu().sum(0).tolist())
+    stats = {"minmax_scans": scans, "sorts": sorts, "replacements": rep, "detected": det, "passes": passes}
+    if rank != 0:
+        return None, stats
+    out = full if ndim == 3 else full[0]
+    if is_tensor:
+        return out.to(orig.device).view(orig.dtype), stats
+    a = out.cpu().numpy()
+    return (a.view(np.uint16) if img.dtype == np.uint16 else a), stats

@@ -175,7 +175,7 @@ def test_gpu_device_shards_match_whole_frame(cuda_ok):
     assert list(tot) == [st.minmax_scans, st.sorts, st.replacements, st.detected]
 
 
-def _cuda_worker(rank, world, port, case, q):
+def _cuda_worker(rank, world, port, case, q, gather=True):
     import torch
     import torch.distributed as dist
 
@@ -189,24 +189,28 @@ def _cuda_worker(rank, world, port, case, q):
         img = generate(scene, nframes=batch)
         if batch == 1:
             img = img[0]
-        out, stats = sharding.run_filter_distributed(img, k, method, passes)  # default: CUDA strips
+        out, stats = sharding.run_filter_distributed(img, k, method, passes, gather=gather)  # CUDA strips / frames
         q.put((rank, None if out is None else out.tobytes(), stats))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("gather", [True, "fused"])
 @pytest.mark.parametrize("case", [("c4", 1, 11, "fnr", 2, 700, 640), ("c2", 6, 5, "fnr", 1, 256, 320),
-                                  ("c3", 1, 7, "mf", 1, 300, 512)])
-def test_gpu_world2_run_filter_distributed(cuda_ok, case):
+                                  ("c3", 1, 7, "mf", 1, 300, 512), ("c5", 5, 3, "fnr", 2, 120, 160)])
+def test_gpu_world2_run_filter_distributed(cuda_ok, case, gather):
     """Two ranks (spawned processes, gloo control plane) filtering their row strips /
-    frame shards with the CUDA kernels reassemble exactly the single-process result."""
+    frame shards with the CUDA kernels reassemble exactly the single-process result —
+    gathered afterwards (torch.distributed.gather) or fused: rank 1's kernels store into
+    rank 0's output through a CUDA IPC mapping (both ranks share the one GPU here, which
+    exercises the same path as NVLink peers)."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_cuda_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    procs = [ctx.Process(target=_cuda_worker, args=(r, 2, port, case, q, gather)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
