@@ -742,16 +742,28 @@ def time_fused_gather(src, dev, rank: int, world: int, share: dict, cfg, lib, _n
     msg = [None]
     if rank == 0:
         handle, off = ctypes.create_string_buffer(64), ctypes.c_uint64(0)
-        _native.check(lib.irdn_ipc_export(full.data_ptr(), handle, ctypes.byref(off)))
-        msg = [(handle.raw, int(off.value))]
+        if lib.irdn_ipc_export(full.data_ptr(), handle, ctypes.byref(off)) == 0:
+            msg = [(handle.raw, int(off.value))]
     dist.broadcast_object_list(msg, src=0)
-    raw, off = msg[0]
-    if rank == 0:
-        base = full.data_ptr()
+    base, why = None, None
+    if msg[0] is None:
+        why = "rank 0 could not export its output buffer"
     else:
-        ptr = ctypes.c_void_p()
-        _native.check(lib.irdn_ipc_open(ctypes.create_string_buffer(raw, 64), off, ctypes.byref(ptr)))
-        base = ptr.value
+        raw, off = msg[0]
+        if rank == 0:
+            base = full.data_ptr()
+        else:
+            ptr = ctypes.c_void_p()
+            if lib.irdn_ipc_open(ctypes.create_string_buffer(raw, 64), off, ctypes.byref(ptr)) == 0:
+                base = ptr.value
+            else:
+                why = _native.load_lib().irdn_last_error().decode()
+    oks = [None] * world
+    dist.all_gather_object(oks, base is not None)  # every rank agrees before any peer store
+    if not all(oks):
+        if base is not None and rank != 0:
+            lib.irdn_ipc_close(ctypes.c_void_p(base), off)
+        return {"unavailable": why or "a peer could not map rank 0's output (no CUDA IPC / P2P)"}
     t = "u8" if bpp == 1 else "u16"
     try:
         def launch():
