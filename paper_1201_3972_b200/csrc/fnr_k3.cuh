@@ -187,8 +187,11 @@ __device__ __forceinline__ void fix_edges(uint8_t* s_in, int gx_lo, int gy_lo, i
 // FULL: every tile of the launch is whole (width % TW == 0, rows % TH == 0): one unmasked
 // tile body. Otherwise the whole tiles still take the unmasked body and only the last
 // column / row of tiles the masked one (a CTA-uniform branch). FNR: method "fnr" (else "mf").
+#ifndef IRDN_K3_MINBLOCKS
+#define IRDN_K3_MINBLOCKS 8  // whole-tile launches: <= 64 registers, 8 CTAs per SM (c5 0.783 -> 0.771 ms; 7 fit at the natural 65)
+#endif
 template <int BAND, bool FULL, bool FNR>
-__global__ void __launch_bounds__(THREADS) fnr_k3_kernel(const __grid_constant__ CUtensorMap in_map,
+__global__ void __launch_bounds__(THREADS, FULL ? IRDN_K3_MINBLOCKS : 5) fnr_k3_kernel(const __grid_constant__ CUtensorMap in_map,
                                                          const tile::TileParams p) {
   using G = Geo<BAND>;
   extern __shared__ __align__(128) uint8_t smem_raw[];
