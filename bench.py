@@ -636,7 +636,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
     alu_lanes = 64 * SM_COUNT * SM_MHZ * 1e6  # thread-instructions / s on the ALU pipe
     so["alu_floor_us"] = round(so["minmax_instr_per_px"] * rank_px / alu_lanes * 1e6, 2)
     so["frac"] = round(so["minmax_instr_per_px"] * rank_px / (kernel_ms * 1e-3) / alu_lanes, 4)
-    if prof.get("instr_per_px"):
+    if prof.get("instr_per_px") and args.method == "fnr" and passes == 1:  # the captures are single FNR passes
         # SM-side floors from the committed capture (instructions / ALU-pipe instructions per pixel)
         ipp, app = prof["instr_per_px"], prof.get("alu_instr_per_px")
         issue_peak = 128 * SM_COUNT * SM_MHZ * 1e6
