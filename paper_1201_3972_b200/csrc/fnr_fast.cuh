@@ -264,7 +264,9 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
                                                                     (long long)sms * blocks_per_sm));
   // Tail: the last `split` full tiles are handed out as two half-height tiles each
   // (about one tile per warp; none when the pool is a single wave).
-  static const double tail_waves = getenv("IRDN_TAIL") ? atof(getenv("IRDN_TAIL")) : 1.0;
+  // (round 1 kept one wave of halves; with the round-2 kernels they cost c2 39.3 vs 37.4 us
+  // and are off by default: IRDN_TAIL=1 restores them)
+  static const double tail_waves = getenv("IRDN_TAIL") ? atof(getenv("IRDN_TAIL")) : 0.0;
   // (a short pool only: with many tiles per warp the tail is a small share and the
   // halves' extra halo rows cost more than they save - c4: 18 tiles/warp, +2 %)
   long long split = wk::WH == 32 ? (long long)(tail_waves * ctas * wk::WARPS) : 0;

@@ -477,11 +477,14 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
   // A prefetch is only a hint (L2 stays coherent with the previous grid's writes), so it
   // is safe even when that grid produces this kernel's input; the smem load itself is
   // issued after griddepcontrol.wait.
-  int first = 0;
+  // The scheduler slot is shared with the previous launch on this stream, which may still be
+  // draining under PDL (its last warp resets the slot), so a dynamically scheduled first tile
+  // (static_rounds == 0: the multi-pass kernel) is claimed only after griddepcontrol.wait.
+  int first = -1;
   if (lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map0) : "memory");
-    first = p.static_rounds > 0 ? gwarp : (int)atomicAdd(p.sched, 1u);
-    if (first < ntiles) {
+    if (p.static_rounds > 0) first = gwarp;
+    if (first >= 0 && first < ntiles) {
       const WTile f = tile_at(first);
       asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(map0),
                    "r"(f.x0 - R), "r"(f.y0 - r - p.in_row0), "r"(f.b)
@@ -498,7 +501,7 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
     for (int s = 0; s < NSTAGE; ++s) tile::mbar_init(&s_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
-    for (int s = 0; s < NSTAGE; ++s) refill(s, s == 0 ? first : -1);
+    for (int s = 0; s < NSTAGE; ++s) refill(s, s == 0 ? first : -1);  // first < 0: from the scheduler
   }
   __syncwarp();
 
