@@ -279,7 +279,7 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   {
     static const int srounds_env = getenv("IRDN_STATIC_ROUNDS") ? atoi(getenv("IRDN_STATIC_ROUNDS")) : -1;
     const long long nwarps = ctas * wk::WARPS;
-    long long sr = srounds_env >= 0 ? srounds_env : 1;
+    long long sr = srounds_env >= 0 ? srounds_env : 2;  // measured: 2 rounds c2 37.36 -> 37.27 us (3: 38.6)
     p.static_rounds = (int)std::max<long long>(0, std::min<long long>(sr, ntiles / nwarps));
     if (srounds_env < 0 && p.static_rounds == 0) p.static_rounds = 1;  // a short pool: one static round
   }
