@@ -27,7 +27,7 @@ template <int K>
 constexpr bool kDense = K == 5 || K == 7;
 
 #ifndef IRDN_WARPS
-#define IRDN_WARPS 2
+#define IRDN_WARPS 4  // round-2 re-sweep: 2 / 4 warps per CTA c2 37.3 / 36.9 us (packaging only)
 #endif
 constexpr int WARPS = IRDN_WARPS;      // warps per CTA (packaging only: no CTA barriers)
 constexpr int THREADS = 32 * WARPS;
@@ -36,7 +36,7 @@ constexpr int WW = 64;                 // warp tile width: 32 lanes x 2 pixels
 #define IRDN_WH 32
 #endif
 #ifndef IRDN_DET_FMA
-#define IRDN_DET_FMA 1  // detector adds / shifts as IMADs on the FMA pipe (0: IADD3 / PRMT / SHF)
+#define IRDN_DET_FMA 0  // odd-offset shifts as PRMT (ALU): round-2 re-sweep c2 37.3 -> 36.4 us (round 1: IMAD)
 #endif
 #ifndef IRDN_WSTAGE
 #define IRDN_WSTAGE 1
@@ -204,7 +204,7 @@ __device__ __forceinline__ void row_minmax(const T* rowp, uint32_t& mn, uint32_t
 // and c4 (11x11) 251.2 -> 253.8 us, so by default only K = 7 pairs its rows
 // (IRDN_VPAIR=0: never, 1: every K).
 #ifndef IRDN_ROWADDR
-#define IRDN_ROWADDR -1  // -1: k <= 5 only (c2 39.93 -> 39.61 us; c3 / c4 0.0 / +0.35 %), 0 never, 1 always
+#define IRDN_ROWADDR 0  // per-row pointer increments (round-2 re-sweep: c2 -0.7 %; -1: k <= 5 only, 1 always)
 #endif
 #ifndef IRDN_VPAIR
 #define IRDN_VPAIR -1
