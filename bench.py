@@ -477,7 +477,7 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
     import torch
 
     from paper_1201_3972_b200 import _native
-    from paper_1201_3972_b200.scene import generate
+    from paper_1201_3972_b200.scene import render_device
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -490,22 +490,28 @@ def run_b200_arm(args, cfg, rank: int, world: int, local: int):
     share = rank_share(cfg, world, rank)
     bpp = cfg.bytes_per_pixel
     H, W = cfg.height, cfg.width
+    # The scene is rendered on the device (irdn_scene_render: the same bytes as the host
+    # generator, tests/test_scene_device.py); the pinned host copy feeds the e2e leg and the
+    # CPU sample.
     if share["kind"] == "frames":
         B = share["f1"] - share["f0"]
-        host = generate(cfg, frame0=share["f0"], nframes=B)
+        d0 = render_device(cfg, frame0=share["f0"], nframes=B, device=local)
         out_rows = H
         rank_px = B * H * W
     else:
         if passes > 1:
             raise SystemExit("row strips (c4 at N > 1) are benchmarked with passes = 1")
         B = 1
-        full = generate(cfg, nframes=1)
-        host = np.ascontiguousarray(full[:, share["in0"]:share["in1"]])
+        full = render_device(cfg, nframes=1, device=local)
+        d0 = full[:, share["in0"]:share["in1"]].contiguous()
         del full
         out_rows = share["y1"] - share["y0"]
         rank_px = out_rows * W
-    h_in = torch.from_numpy(host).pin_memory() if bpp == 1 else torch.from_numpy(host.view(np.int16)).pin_memory()
-    d0 = h_in.to(dev, non_blocking=False)  # u16 pixels travel as int16 bit patterns
+    if bpp == 2:
+        d0 = d0.view(torch.int16)  # u16 pixels travel as int16 bit patterns
+    h_in = torch.empty(d0.shape, dtype=d0.dtype, pin_memory=True)
+    h_in.copy_(d0)
+    host = h_in.numpy() if bpp == 1 else h_in.numpy().view(np.uint16)
     in_bytes = d0.numel() * bpp
     out_shape = (B, out_rows, W)
     R = max(1, math.ceil(2 * L2_BYTES / (in_bytes + rank_px * bpp)))

@@ -18,6 +18,8 @@
  *                                    noise.py:17-34; bit-identical output image, mask and count)
  *   irdn_sq_err_sum_u8 / _u16     <- metrics.py:22-32    the exact integer sum inside mse() (and psnr(),
  *                                    quality_report(), build_comparison())
+ *   irdn_scene_render             <- (no reference interface) the seeded BASELINE scenes of
+ *                                    csrc/scene.c rendered on the device (bench / test input)
  *
  * Semantics (bit-exact with the reference):
  *   - row-major frames, origin top-left; replicate-edge (clamp) window gather;
@@ -166,6 +168,32 @@ IRDN_API int irdn_sq_err_sum_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t 
                                 unsigned long long* d_sum, void* stream);
 IRDN_API int irdn_sq_err_sum_u16(const uint16_t* d_a, const uint16_t* d_b, int64_t n,
                                  unsigned long long* d_sum, void* stream);
+
+/*
+ * Seeded BASELINE scene rendering on the device (bench / test input, SURVEY §8f rank 2;
+ * not a reference interface: the reference evaluates on one IR photograph, SPEC.md:309,
+ * that these scenes stand in for). Renders frames [frame0, frame0 +
+ * nframes) of the scene csrc/scene.c's scene_generate() defines into d_out (contiguous
+ * [nframes][height][width] pixels of bytes_per_pixel bytes), stream-ordered, byte for byte
+ * equal to scene_generate(). The tables are scene_tables()' output (the per-frame
+ * parameters that need exp / sin / cos, computed by the host code), copied to the device.
+ */
+typedef struct irdn_scene_desc {
+  int32_t width, height, bytes_per_pixel, maxval;
+  int32_t nblobs, nlines, nrects;  /* nlines <= 64, nrects <= 256 (scene.c's caps) */
+  int32_t impulse_kind;            /* 0 none, 1 salt & pepper, 2 uniform random */
+  int32_t config_id, sensor;       /* sensor: 1 iff sensor_sigma > 0 */
+  double scale;                    /* maxval / 255.0 */
+  double sensor_mul;               /* sensor_sigma * 1.7320508075688772 */
+  double line_amp, rect_amp, density;
+  uint64_t seed;
+  int64_t frame0, nframes;         /* height and nframes <= 65535 per call */
+  const double* gx;                /* [nframes][nblobs][width]  device */
+  const double* gy;                /* [nframes][nblobs][height] device */
+  const double* lines;             /* [nframes][nlines][5]      device */
+  const int32_t* rects;            /* [nframes][nrects][4]      device, 16-byte aligned */
+} irdn_scene_desc;
+IRDN_API int irdn_scene_render(const irdn_scene_desc* desc, void* d_out, void* stream);
 
 /*
  * passes > 1 (irdn_run_filter_*, irdn_run_filter_device_*): 1 = all passes in ONE

@@ -50,10 +50,24 @@ EXPORTED = [
     "irdn_set_force_generic", "irdn_inject_impulse_u8", "irdn_sq_err_sum_u8", "irdn_sq_err_sum_u16",
     "irdn_set_host_return", "irdn_last_transfer", "irdn_delta_region_bytes", "irdn_delta_encode_u8",
     "irdn_delta_encode_u16", "irdn_delta_decode_u8", "irdn_delta_decode_u16", "irdn_set_multipass",
-    "irdn_ipc_export", "irdn_ipc_open", "irdn_ipc_close",
+    "irdn_ipc_export", "irdn_ipc_open", "irdn_ipc_close", "irdn_scene_render",
 ]
 
 HOST_RETURN = {"auto": 0, "full": 1, "delta": 2}
+
+
+class IrdnSceneDesc(ctypes.Structure):
+    """irdn_scene_desc (include/irdn.h)."""
+
+    _fields_ = [
+        ("width", ctypes.c_int32), ("height", ctypes.c_int32), ("bytes_per_pixel", ctypes.c_int32),
+        ("maxval", ctypes.c_int32), ("nblobs", ctypes.c_int32), ("nlines", ctypes.c_int32),
+        ("nrects", ctypes.c_int32), ("impulse_kind", ctypes.c_int32), ("config_id", ctypes.c_int32),
+        ("sensor", ctypes.c_int32), ("scale", ctypes.c_double), ("sensor_mul", ctypes.c_double),
+        ("line_amp", ctypes.c_double), ("rect_amp", ctypes.c_double), ("density", ctypes.c_double),
+        ("seed", ctypes.c_uint64), ("frame0", ctypes.c_int64), ("nframes", ctypes.c_int64),
+        ("gx", ctypes.c_void_p), ("gy", ctypes.c_void_p), ("lines", ctypes.c_void_p), ("rects", ctypes.c_void_p),
+    ]
 
 
 def _declare(l: ctypes.CDLL) -> None:
@@ -105,6 +119,8 @@ def _declare(l: ctypes.CDLL) -> None:
     l.irdn_ipc_open.argtypes = [vp, u64, ctypes.POINTER(vp)]
     l.irdn_ipc_close.restype = ctypes.c_int
     l.irdn_ipc_close.argtypes = [vp, u64]
+    l.irdn_scene_render.restype = ctypes.c_int
+    l.irdn_scene_render.argtypes = [ctypes.POINTER(IrdnSceneDesc), vp, vp]
     l.irdn_delta_region_bytes.restype = u64
     l.irdn_delta_region_bytes.argtypes = [i64, i32]
     for t in ("u8", "u16"):
@@ -142,6 +158,9 @@ def load_scene_lib() -> ctypes.CDLL:
             l.scene_generate.restype = ctypes.c_int
             l.scene_generate.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                          ctypes.c_void_p, ctypes.c_int32]
+            l.scene_tables.restype = ctypes.c_int
+            l.scene_tables.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
             _scene = l
     return _scene
 

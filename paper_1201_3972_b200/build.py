@@ -18,7 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CUDA_SOURCES = ["irdn_api.cu", "delta_host.cpp"]
 CUDA_HEADERS = ["fnr_common.cuh", "fnr_generic.cuh", "fnr_fast.cuh", "fnr_tile.cuh",
-                "select_nets.cuh", "sep_nets.cuh", "fnr_dense.cuh", "fnr_k3.cuh", "fnr_warp.cuh", "noise.cuh", "metrics.cuh", "delta.cuh", "fnr_large.cuh"]
+                "select_nets.cuh", "sep_nets.cuh", "fnr_dense.cuh", "fnr_k3.cuh", "fnr_warp.cuh", "noise.cuh", "metrics.cuh", "delta.cuh", "fnr_large.cuh", "scene.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -59,7 +59,7 @@ def build_scene(force: bool = False) -> str:
     target = os.path.join(PKG_DIR, "libirdn_scene.so")
     src = os.path.join(CSRC, "scene.c")
     if force or _stale(target, [src]):
-        cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fvisibility=hidden",
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-std=c11", "-fPIC", "-shared", "-fvisibility=hidden",
                "-D_GNU_SOURCE", "-o", target, src, "-lm", "-lpthread"]
         subprocess.run(cmd, check=True)
     return target

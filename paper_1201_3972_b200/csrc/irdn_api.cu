@@ -26,6 +26,7 @@
 #include "fnr_fast.cuh"
 #include "metrics.cuh"
 #include "noise.cuh"
+#include "scene.cuh"
 #include "delta.cuh"
 #include "fnr_large.cuh"
 
@@ -970,6 +971,15 @@ int irdn_sq_err_sum_u8(const uint8_t* d_a, const uint8_t* d_b, int64_t n, unsign
 int irdn_sq_err_sum_u16(const uint16_t* d_a, const uint16_t* d_b, int64_t n, unsigned long long* d_sum,
                         void* stream) {
   return sq_err_sum<uint16_t>(d_a, d_b, n, d_sum, stream);
+}
+int irdn_scene_render(const irdn_scene_desc* desc, void* d_out, void* stream) {
+  int rc = check_device(nullptr);
+  if (rc != IRDN_OK) return rc;
+  cudaError_t err = cudaSuccess;
+  rc = scene::render(desc, d_out, static_cast<cudaStream_t>(stream), &err);
+  if (rc == IRDN_EINVAL) return fail(rc, "invalid scene descriptor");
+  if (rc != IRDN_OK) return fail(rc, "scene render launch failed: %s", cudaGetErrorString(err));
+  return IRDN_OK;
 }
 int32_t irdn_set_multipass(int32_t on) {
   int32_t prev = g_multipass;

@@ -68,14 +68,9 @@ typedef struct {
   int32_t band_rows;
 } job_t;
 
-static void gen_band(const scene_params* p, int64_t f, int32_t y0, int32_t y1, void* frame_out) {
+/* Blob parameters of frame f and the horizontal Gaussian factors gx[j * W + x]. */
+static void frame_blobs(const scene_params* p, int64_t f, double* gx, double* amp, double* cyv, double* sgv) {
   const int32_t W = p->width, H = p->height, nb = p->nblobs;
-  const double scale = (double)p->maxval / 255.0;
-  double* gx = (double*)malloc(sizeof(double) * (size_t)nb * W);
-  double* amp = (double*)malloc(sizeof(double) * (size_t)nb);
-  double* cyv = (double*)malloc(sizeof(double) * (size_t)nb);
-  double* sgv = (double*)malloc(sizeof(double) * (size_t)nb);
-  double* rowv = (double*)malloc(sizeof(double) * (size_t)W);
   for (int j = 0; j < nb; ++j) {
     /* drifting blobs keep one parameter set for the whole sequence (frame key 0) */
     const uint64_t fk = p->drift ? 0 : (uint64_t)f;
@@ -94,9 +89,19 @@ static void gen_band(const scene_params* p, int64_t f, int32_t y0, int32_t y1, v
     const double inv = 1.0 / (2.0 * s * s);
     for (int32_t x = 0; x < W; ++x) gx[(size_t)j * W + x] = exp(-(x - cx) * (x - cx) * inv);
   }
-  /* line and rectangle parameters for this frame */
-  double lsin[64], lcos[64], lpx[64], lpy[64], lhw[64];
-  int32_t nl = p->nlines > 64 ? 64 : p->nlines;
+}
+
+/* Vertical factor of blob (amp, cy, s) at row y (the blob's weight on that row). */
+static inline double blob_gy(double amp, double cy, double s, int32_t y) {
+  const double dy = y - cy;
+  return amp * exp(-dy * dy / (2.0 * s * s));
+}
+
+/* Hot lines of frame f: sin, cos, anchor x, anchor y, half width (n <= 64). */
+static int32_t frame_lines(const scene_params* p, int64_t f, double* lsin, double* lcos, double* lpx, double* lpy,
+                           double* lhw) {
+  const int32_t W = p->width, H = p->height;
+  const int32_t nl = p->nlines > 64 ? 64 : p->nlines;
   for (int i = 0; i < nl; ++i) {
     double th = 3.141592653589793 * u01(key(p, (uint64_t)f, ST_LINE, (uint64_t)i * 8 + 0));
     lsin[i] = sin(th);
@@ -105,8 +110,13 @@ static void gen_band(const scene_params* p, int64_t f, int32_t y0, int32_t y1, v
     lpy[i] = u01(key(p, (uint64_t)f, ST_LINE, (uint64_t)i * 8 + 2)) * H;
     lhw[i] = 0.5 * (double)(1 + (int)(3.0 * u01(key(p, (uint64_t)f, ST_LINE, (uint64_t)i * 8 + 3))));
   }
-  int32_t nr = p->nrects > 256 ? 256 : p->nrects;
-  int32_t rx0[256], ry0[256], rx1[256], ry1[256];
+  return nl;
+}
+
+/* Text-like rectangles of frame f as half-open [x0, x1) x [y0, y1) (n <= 256). */
+static int32_t frame_rects(const scene_params* p, int64_t f, int32_t* rx0, int32_t* ry0, int32_t* rx1, int32_t* ry1) {
+  const int32_t W = p->width, H = p->height;
+  const int32_t nr = p->nrects > 256 ? 256 : p->nrects;
   for (int i = 0; i < nr; ++i) {
     int32_t rw = 6 + (int32_t)(7.0 * u01(key(p, (uint64_t)f, ST_RECT, (uint64_t)i * 8 + 0)));
     int32_t rh = 6 + (int32_t)(7.0 * u01(key(p, (uint64_t)f, ST_RECT, (uint64_t)i * 8 + 1)));
@@ -116,12 +126,28 @@ static void gen_band(const scene_params* p, int64_t f, int32_t y0, int32_t y1, v
     rx1[i] = rx0[i] + rw;
     ry1[i] = ry0[i] + rh;
   }
+  return nr;
+}
+
+static void gen_band(const scene_params* p, int64_t f, int32_t y0, int32_t y1, void* frame_out) {
+  const int32_t W = p->width, nb = p->nblobs;
+  const double scale = (double)p->maxval / 255.0;
+  double* gx = (double*)malloc(sizeof(double) * (size_t)nb * W);
+  double* amp = (double*)malloc(sizeof(double) * (size_t)nb);
+  double* cyv = (double*)malloc(sizeof(double) * (size_t)nb);
+  double* sgv = (double*)malloc(sizeof(double) * (size_t)nb);
+  double* rowv = (double*)malloc(sizeof(double) * (size_t)W);
+  frame_blobs(p, f, gx, amp, cyv, sgv);
+  /* line and rectangle parameters for this frame */
+  double lsin[64], lcos[64], lpx[64], lpy[64], lhw[64];
+  const int32_t nl = frame_lines(p, f, lsin, lcos, lpx, lpy, lhw);
+  int32_t rx0[256], ry0[256], rx1[256], ry1[256];
+  const int32_t nr = frame_rects(p, f, rx0, ry0, rx1, ry1);
   const double sens = p->sensor_sigma * 1.7320508075688772; /* sqrt(12/4) */
   for (int32_t y = y0; y < y1; ++y) {
     for (int32_t x = 0; x < W; ++x) rowv[x] = 60.0;
     for (int j = 0; j < nb; ++j) {
-      const double dy = y - cyv[j];
-      const double gy = amp[j] * exp(-dy * dy / (2.0 * sgv[j] * sgv[j]));
+      const double gy = blob_gy(amp[j], cyv[j], sgv[j], y);
       if (gy < 1e-6) continue;
       const double* g = gx + (size_t)j * W;
       for (int32_t x = 0; x < W; ++x) rowv[x] += gy * g[x];
@@ -197,6 +223,87 @@ SCENE_EXPORT int scene_generate(const scene_params* p, int64_t frame0, int64_t n
   if (nthreads == 1) job_main(&jobs[0]);
   else {
     for (int i = 0; i < nthreads; ++i) pthread_create(&tids[i], NULL, job_main, &jobs[i]);
+    for (int i = 0; i < nthreads; ++i) pthread_join(tids[i], NULL);
+  }
+  free(jobs);
+  free(tids);
+  return 0;
+}
+
+/*
+ * The per-frame parameter tables of frames [frame0, frame0 + nframes) for the device
+ * generator (csrc/scene.cuh): everything above that needs exp / sin / cos, computed by the
+ * same code gen_band runs, so the device (IEEE +, *, rint in gen_band's order) writes the
+ * same bytes as scene_generate. Layout per frame i:
+ *   gx    [i][nblobs][width]   horizontal Gaussian factor of blob j at column x
+ *   gy    [i][nblobs][height]  amplitude x vertical factor of blob j at row y
+ *   lines [i][nl][5]           sin, cos, anchor x, anchor y, half width (nl = min(nlines, 64))
+ *   rects [i][nr][4]           x0, y0, x1, y1 (half-open; nr = min(nrects, 256))
+ * lines / rects may be NULL when nlines / nrects is 0.
+ */
+typedef struct {
+  const scene_params* p;
+  int64_t frame0, i0, i1;
+  double *gx, *gy, *lines;
+  int32_t* rects;
+} tab_job_t;
+
+static void* tab_main(void* arg) {
+  const tab_job_t* t = (const tab_job_t*)arg;
+  const scene_params* p = t->p;
+  const int32_t W = p->width, H = p->height, nb = p->nblobs;
+  const int32_t nl = p->nlines > 64 ? 64 : p->nlines, nr = p->nrects > 256 ? 256 : p->nrects;
+  double* amp = (double*)malloc(sizeof(double) * (size_t)(nb > 0 ? nb : 1));
+  double* cyv = (double*)malloc(sizeof(double) * (size_t)(nb > 0 ? nb : 1));
+  double* sgv = (double*)malloc(sizeof(double) * (size_t)(nb > 0 ? nb : 1));
+  for (int64_t i = t->i0; i < t->i1; ++i) {
+    const int64_t f = t->frame0 + i;
+    frame_blobs(p, f, t->gx + (size_t)i * nb * W, amp, cyv, sgv);
+    double* gy = t->gy + (size_t)i * nb * H;
+    for (int j = 0; j < nb; ++j)
+      for (int32_t y = 0; y < H; ++y) gy[(size_t)j * H + y] = blob_gy(amp[j], cyv[j], sgv[j], y);
+    if (nl > 0 && t->lines) {
+      double lsin[64], lcos[64], lpx[64], lpy[64], lhw[64];
+      frame_lines(p, f, lsin, lcos, lpx, lpy, lhw);
+      double* L = t->lines + (size_t)i * nl * 5;
+      for (int k = 0; k < nl; ++k) {
+        L[5 * k + 0] = lsin[k];
+        L[5 * k + 1] = lcos[k];
+        L[5 * k + 2] = lpx[k];
+        L[5 * k + 3] = lpy[k];
+        L[5 * k + 4] = lhw[k];
+      }
+    }
+    if (nr > 0 && t->rects) {
+      int32_t rx0[256], ry0[256], rx1[256], ry1[256];
+      frame_rects(p, f, rx0, ry0, rx1, ry1);
+      int32_t* R = t->rects + (size_t)i * nr * 4;
+      for (int k = 0; k < nr; ++k) {
+        R[4 * k + 0] = rx0[k];
+        R[4 * k + 1] = ry0[k];
+        R[4 * k + 2] = rx1[k];
+        R[4 * k + 3] = ry1[k];
+      }
+    }
+  }
+  free(amp); free(cyv); free(sgv);
+  return NULL;
+}
+
+SCENE_EXPORT int scene_tables(const scene_params* p, int64_t frame0, int64_t nframes, double* gx, double* gy,
+                              double* lines, int32_t* rects, int32_t nthreads) {
+  if (!p || p->width < 1 || p->height < 1 || nframes < 0 || p->nblobs < 0 || (p->nblobs > 0 && (!gx || !gy)))
+    return 1;
+  if (nthreads < 1) nthreads = 1;
+  if ((int64_t)nthreads > nframes) nthreads = (int32_t)(nframes > 0 ? nframes : 1);
+  tab_job_t* jobs = (tab_job_t*)calloc((size_t)nthreads, sizeof(tab_job_t));
+  pthread_t* tids = (pthread_t*)calloc((size_t)nthreads, sizeof(pthread_t));
+  for (int i = 0; i < nthreads; ++i) {
+    jobs[i] = (tab_job_t){p, frame0, nframes * i / nthreads, nframes * (i + 1) / nthreads, gx, gy, lines, rects};
+  }
+  if (nthreads == 1) tab_main(&jobs[0]);
+  else {
+    for (int i = 0; i < nthreads; ++i) pthread_create(&tids[i], NULL, tab_main, &jobs[i]);
     for (int i = 0; i < nthreads; ++i) pthread_join(tids[i], NULL);
   }
   free(jobs);

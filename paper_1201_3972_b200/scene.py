@@ -122,3 +122,63 @@ def generate(cfg: SceneConfig, frame0: int = 0, nframes: int | None = None, seed
     if rc != 0:
         raise ValueError("scene_generate rejected the parameters")
     return out
+
+
+def tables(cfg: SceneConfig, frame0: int = 0, nframes: int | None = None, seed: int = SEED,
+           threads: int | None = None) -> dict:
+    """The per-frame scene parameters that need exp / sin / cos (csrc/scene.c scene_tables):
+    gx [n, nblobs, W], gy [n, nblobs, H] (float64), lines [n, nl, 5], rects [n, nr, 4] (int32)."""
+    n = cfg.frames if nframes is None else nframes
+    nl, nr = min(cfg.nlines, 64), min(cfg.nrects, 256)
+    t = {
+        "gx": np.empty((n, cfg.nblobs, cfg.width), np.float64),
+        "gy": np.empty((n, cfg.nblobs, cfg.height), np.float64),
+        "lines": np.empty((n, nl, 5), np.float64),
+        "rects": np.empty((n, nr, 4), np.int32),
+    }
+    p = cfg.params(seed)
+    nt = threads or max(1, min(32, os.cpu_count() or 1))
+    rc = load_scene_lib().scene_tables(
+        ctypes.byref(p), frame0, n, t["gx"].ctypes.data, t["gy"].ctypes.data,
+        t["lines"].ctypes.data if nl else None, t["rects"].ctypes.data if nr else None, nt)
+    if rc != 0:
+        raise ValueError("scene_tables rejected the parameters")
+    return t
+
+
+def render_device(cfg: SceneConfig, frame0: int = 0, nframes: int | None = None, seed: int = SEED,
+                  out=None, device=None, chunk_bytes: int = 64 << 20):
+    """Frames [frame0, frame0+nframes) of `cfg` rendered on the GPU (irdn_scene_render) as a
+    CUDA tensor [B, H, W] (torch.uint8 / torch.uint16), byte for byte equal to generate(). The per-frame exp / sin / cos tables come from the host
+    (tables()), a chunk of frames at a time, on the current torch stream."""
+    import torch
+
+    from . import _native
+
+    lib = _native.load_lib()
+    n = cfg.frames if nframes is None else nframes
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    tdt = torch.uint8 if cfg.dtype == "u8" else torch.uint16
+    if out is None:
+        out = torch.empty((n, cfg.height, cfg.width), dtype=tdt, device=dev)
+    if out.dtype != tdt or not out.is_contiguous() or out.numel() != n * cfg.height * cfg.width:
+        raise ValueError("out must be a contiguous CUDA tensor of the scene's dtype and shape")
+    nl, nr = min(cfg.nlines, 64), min(cfg.nrects, 256)
+    per_frame = 8 * cfg.nblobs * (cfg.width + cfg.height) + 40 * nl + 16 * nr + 1
+    chunk = max(1, min(65535, chunk_bytes // per_frame))
+    stream = torch.cuda.current_stream(dev)
+    flat = out.view(n, -1)
+    for c0 in range(0, n, chunk):
+        c = min(chunk, n - c0)
+        t = tables(cfg, frame0 + c0, c, seed)
+        dt = {k: torch.from_numpy(v).to(dev, non_blocking=False) for k, v in t.items()}
+        d = _native.IrdnSceneDesc(
+            cfg.width, cfg.height, cfg.bytes_per_pixel, cfg.maxval, cfg.nblobs, nl, nr,
+            {"none": 0, "sp": 1, "uniform": 2}[cfg.impulse], cfg.config_id, int(cfg.sensor_sigma > 0),
+            cfg.maxval / 255.0, cfg.sensor_sigma * 1.7320508075688772, cfg.line_amp, cfg.rect_amp,
+            cfg.density, seed, frame0 + c0, c,
+            dt["gx"].data_ptr(), dt["gy"].data_ptr(), dt["lines"].data_ptr() if nl else None,
+            dt["rects"].data_ptr() if nr else None)
+        _native.check(lib.irdn_scene_render(ctypes.byref(d), flat[c0].data_ptr(), stream.cuda_stream))
+        stream.synchronize()  # the chunk's tables are freed at the end of this iteration
+    return out
