@@ -146,8 +146,8 @@ def job_pixels(cfg, world: int) -> int:
 #   dense 3x3 (fnr_k3.cuh, 16 output columns + 2 halo columns per thread):
 #     column sort 2 x 18/16, window min/max of column lows/highs 4, median of the three
 #     column middles 3 (sorted shared pair + clamp), final median-of-3 2
-#   warp kernel k = 5..11 (fnr_warp.cuh, 64 x 32 tiles, pixel pairs): detector
-#     (K-1)(1 + 2r/32) horizontal + (K-1) vertical + 1 flag test per pair, plus the median
+#   warp kernel k = 5..11 (fnr_warp.cuh, 64 x 32 tiles, 64 x 48 for k = 11, pixel pairs): detector
+#     (K-1)(1 + 2r/rows) horizontal + (K-1) vertical + 1 flag test per pair, plus the median
 #     network for two flagged pixels (select_nets.cuh) times the detected fraction.
 NET_INSTR_PER_PAIR = {3: 30, 5: 172, 7: 514, 9: None, 11: 1833}
 # dense median stage (fnr_dense.cuh, sep_nets.cuh; k = 5 / 7): VIMNMX instructions per output
@@ -169,7 +169,8 @@ def static_ops(cfg, detected_fraction: float, method: str = "fnr") -> dict:
                 "minmax_lane_ops_per_px": round(per_pair, 3),
                 "note": "VIMNMX(3).U16x2 instructions per pixel (each covers 2 pixels); lane ops per pixel"}
     K, r = cfg.k, cfg.k // 2
-    det = (K - 1) * (1 + 2 * r / 32) + (K - 1) + 1
+    tile_rows = 48 if K >= 11 else 32  # fnr_warp.cuh WHK<K>
+    det = (K - 1) * (1 + 2 * r / tile_rows) + (K - 1) + 1
     net = NET_INSTR_PER_PAIR.get(K)
     dense = DENSE_INSTR_PER_PAIR.get(K)
     if dense is not None and (method == "mf" or detected_fraction > DENSE_FRAC[K]):

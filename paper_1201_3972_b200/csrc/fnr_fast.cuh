@@ -170,7 +170,7 @@ inline int dense_min_for() {
   // 64 x 640x512 frames, salt-and-pepper density swept): 5x5 ~20 % flagged, 7x7 ~18 %
   const double frac = env > -2.0 ? env : (K == 7 ? 0.18 : 0.20);
   if (frac < 0.0) return -1;
-  return (int)(frac * wk::WW * wk::WH);
+  return (int)(frac * wk::WW * wk::WHK<K>);
 }
 inline unsigned int* sched_slot(int dev, cudaStream_t s) {
   struct Entry { int dev; cudaStream_t s; unsigned int slot; };
@@ -243,7 +243,7 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   p.row_begin = g.row_begin;
   p.row_end = g.row_end;
   p.tiles_x = (g.width + wk::WW - 1) / wk::WW;
-  p.tiles_y = (out_rows + wk::WH - 1) / wk::WH;
+  p.tiles_y = (out_rows + G::TH - 1) / G::TH;
   p.batch = g.batch;
   p.method = method;
   p.counts = counts;
@@ -269,7 +269,7 @@ inline int launch_warp(const T* d_in, T* d_out, const PassGeom& g, int method, u
   static const double tail_waves = getenv("IRDN_TAIL") ? atof(getenv("IRDN_TAIL")) : 0.0;
   // (a short pool only: with many tiles per warp the tail is a small share and the
   // halves' extra halo rows cost more than they save - c4: 18 tiles/warp, +2 %)
-  long long split = wk::WH == 32 ? (long long)(tail_waves * ctas * wk::WARPS) : 0;
+  long long split = G::TH % 32 == 0 ? (long long)(tail_waves * ctas * wk::WARPS) : 0;
   if (ntiles <= ctas * wk::WARPS || ntiles >= 8LL * ctas * wk::WARPS) split = 0;
   split = std::min(split, ntiles);
   p.full_tiles = (int)(ntiles - split);
@@ -374,7 +374,7 @@ inline int launch_warp_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, 
   p.row_begin = g.row_begin;
   p.row_end = g.row_end;
   p.tiles_x = (g.width + wk::WW - 1) / wk::WW;
-  p.tiles_y = (g.row_end - g.row_begin + wk::WH - 1) / wk::WH;
+  p.tiles_y = (g.row_end - g.row_begin + G::TH - 1) / G::TH;
   p.batch = g.batch;
   p.method = method;
   p.counts = counts;
@@ -394,7 +394,7 @@ inline int launch_warp_mp(const T* d_in, T* d_out, T* d_tmp, const PassGeom& g, 
   const long long ctas = std::max<long long>(1, std::min<long long>((npass + wk::WARPS - 1) / wk::WARPS,
                                                                     (long long)sms * blocks_per_sm));
   const long long nwarps = ctas * wk::WARPS;
-  long long split = wk::WH == 32 ? nwarps : 0;  // half-height tail: about one tile per warp
+  long long split = G::TH % 32 == 0 ? nwarps : 0;  // half-height tail: about one tile per warp
   if ((long long)passes * npass <= nwarps || (long long)passes * npass >= 8LL * nwarps) split = 0;
   split = std::min(split, npass);
   p.full_tiles = (int)(npass - split);

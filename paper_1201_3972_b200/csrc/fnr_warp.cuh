@@ -15,6 +15,7 @@
 // Frame borders: TMA zero-fills out-of-frame cells; the warp overwrites them with the
 // nearest in-frame cell (replicate edge, image.py:117-130) before filtering.
 #pragma once
+#include <type_traits>
 #include "fnr_tile.cuh"
 #include "fnr_dense.cuh"
 
@@ -41,8 +42,17 @@ constexpr int WW = 64;                 // warp tile width: 32 lanes x 2 pixels
 #ifndef IRDN_WSTAGE
 #define IRDN_WSTAGE 1
 #endif
-constexpr int WH = IRDN_WH;            // warp tile height (16 or 32: one flag word per 16 rows)
+constexpr int WH = IRDN_WH;            // warp tile height, k <= 9 (16 or 32: one flag word per 16 rows)
 constexpr int NSTAGE = IRDN_WSTAGE;
+// k >= 11: taller tiles. The median stage runs one 121-input network per lane for up to 64
+// queued pixels whatever their number, and BASELINE c4 flags ~1.7 % of its pixels: a 64 x 32
+// tile queues ~34 (17 of 32 lanes busy), a 64 x 48 tile ~51 (26 lanes) and still fits one
+// round; the halo rows fall from 42 / 32 to 58 / 48.
+#ifndef IRDN_WH11
+#define IRDN_WH11 48
+#endif
+template <int K>
+constexpr int WHK = K >= 11 ? IRDN_WH11 : WH;
 #ifndef IRDN_QCAP
 #define IRDN_QCAP 2048
 #endif
@@ -57,7 +67,10 @@ struct Geo {
   static constexpr int R = A;
   static_assert(r <= R, "window radius exceeds the aligned halo");
   static constexpr int BOXW = ((WW + R + r + A - 1) / A) * A;
-  static constexpr int BOXH = WH + 2 * r;
+  static constexpr int TH = WHK<K>;      // warp tile height
+  static constexpr int NF = (TH + 15) / 16;  // flag words per lane (16 rows x 2 pixels each)
+  static_assert(TH % 16 == 0 && TH >= 16 && TH <= 64, "whole 16-row flag words, 8-bit queue rows");
+  static constexpr int BOXH = TH + 2 * r;
   static constexpr int IN_BYTES = BOXW * BOXH * (int)sizeof(T);
   static constexpr int STAGE = (IN_BYTES + 127) & ~127;
   static constexpr int Q_OFF = NSTAGE * STAGE;
@@ -75,32 +88,34 @@ struct WTile {
 // ntiles - full_tiles full tiles, p.full_tiles.. onwards), so the warps that finish
 // last finish a short tile: with ~3.5 tiles per warp the tail of a 64 x 32 pool is
 // about one tile time.
+template <int TH>
 __device__ __forceinline__ WTile tile_of(const tile::TileParams& p, int t, int tiles_per_frame) {
   WTile ti;
   ti.t = t;
-  int f = t, rows = WH, dy = 0;
+  int f = t, rows = TH, dy = 0;
   if (t >= p.full_tiles) {
     const int h = t - p.full_tiles;
     f = p.full_tiles + (h >> 1);
-    rows = WH / 2;
-    dy = (h & 1) * (WH / 2);
+    rows = TH / 2;
+    dy = (h & 1) * (TH / 2);
   }
   ti.b = tile::udiv(f, tiles_per_frame, p.tpf_magic);
   const int tt = f - ti.b * tiles_per_frame;
   const int ty = tile::udiv(tt, p.tiles_x, p.tx_magic);
   ti.x0 = (tt - ty * p.tiles_x) * WW;
-  ti.y0 = p.row_begin + ty * WH + dy;
+  ti.y0 = p.row_begin + ty * TH + dy;
   ti.rows = rows;
   return ti;
 }
 
 // Multi-pass launch: tiles [0, (P-1) N) are the full tiles of passes 0 .. P-2 in order
 // (N tiles per pass), the rest is the last pass with its half-height tail (tile_of).
+template <int TH>
 __device__ __forceinline__ WTile tile_of_mp(const tile::TileParams& p, int t, int tiles_per_frame) {
   const int N = tiles_per_frame * p.batch;
   const int early = (p.passes - 1) * N;
   if (t >= early) {
-    WTile ti = tile_of(p, t - early, tiles_per_frame);
+    WTile ti = tile_of<TH>(p, t - early, tiles_per_frame);
     ti.t = t;
     ti.pass = p.passes - 1;
     return ti;
@@ -113,8 +128,8 @@ __device__ __forceinline__ WTile tile_of_mp(const tile::TileParams& p, int t, in
   const int tt = u - ti.b * tiles_per_frame;
   const int ty = tt / p.tiles_x;
   ti.x0 = (tt - ty * p.tiles_x) * WW;
-  ti.y0 = p.row_begin + ty * WH;
-  ti.rows = WH;
+  ti.y0 = p.row_begin + ty * TH;
+  ti.rows = TH;
   return ti;
 }
 
@@ -209,10 +224,10 @@ __device__ __forceinline__ void row_minmax(const T* rowp, uint32_t& mn, uint32_t
 #ifndef IRDN_VPAIR
 #define IRDN_VPAIR -1
 #endif
-template <typename T, int K, bool FULL, int ROWS = WH>
+template <typename T, int K, bool FULL, int ROWS = WHK<K>>
 __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t pitch, int valid_rows, bool ok0,
                                        bool ok1, uint32_t (&flags)[2], uint32_t one) {
-  static_assert(WH == 16 || WH == 32, "one or two 16-row flag words");
+  static_assert(ROWS <= 32, "one or two 16-row flag words (taller tiles: detect_rolled)");
   static_assert(ROWS % 2 == 0, "output rows are produced in pairs");
   using G = Geo<T, K>;
   constexpr int r = G::r, BOXW = G::BOXW;
@@ -280,10 +295,10 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
 #ifndef IRDN_ROLLED_MIN_K
 #define IRDN_ROLLED_MIN_K 11
 #endif
-template <typename T, int K, bool FULL, int ROWS = WH>
+template <typename T, int K, bool FULL, int ROWS = WHK<K>>
 __device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, int64_t pitch, int valid_rows,
-                                              bool ok0, bool ok1, uint32_t (&flags)[2], uint32_t one) {
-  static_assert(ROWS <= 32, "flag streams hold 32 rows");
+                                              bool ok0, bool ok1, uint32_t (&flags)[Geo<T, K>::NF], uint32_t one) {
+  static_assert(ROWS <= 64, "flag streams hold 64 rows");
   using G = Geo<T, K>;
   constexpr int r = G::r, BOXW = G::BOXW;
   constexpr int J = (r + 1) / 2;
@@ -311,7 +326,9 @@ __device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, in
     }
     hn[0] = hx[0] = cp[0] = 0u;
   }
-  uint32_t st0 = 0u, st1 = 0u;  // signal streams: bit y = row y of pixel 0 / pixel 1 is not noisy
+  // signal streams: bit y = row y of pixel 0 / pixel 1 is not noisy
+  using Stream = std::conditional_t<(ROWS > 32), uint64_t, uint32_t>;
+  Stream st0 = 0u, st1 = 0u;
   T* orow = outp;
 #pragma unroll 1
   for (int b = 0; b < NB; ++b) {
@@ -334,8 +351,8 @@ __device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, in
       }
     }
     constexpr uint32_t kBlk = (1u << K) - 1u;
-    st0 |= (blk & kBlk) << (b * K);
-    st1 |= ((blk >> 16) & kBlk) << (b * K);
+    st0 |= (Stream)(blk & kBlk) << (b * K);
+    st1 |= (Stream)((blk >> 16) & kBlk) << (b * K);
     hn[K - 1] = cn[K - 1];
     hx[K - 1] = cx[K - 1];
 #pragma unroll
@@ -346,12 +363,15 @@ __device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, in
 #pragma unroll
     for (int i = 0; i < K; ++i) cp[i] = cc[i];
   }
-  constexpr uint32_t kRows = ROWS >= 32 ? 0xFFFFFFFFu : (1u << ROWS) - 1u;
+  constexpr Stream kRows = ROWS >= 8 * (int)sizeof(Stream) ? ~(Stream)0 : ((Stream)1 << (ROWS % 64)) - 1u;
   st0 = ~st0 & kRows;  // noisy streams
   st1 = ~st1 & kRows;
   // detect()'s layout: row y at bits y % 16 (pixel 0) and 16 + y % 16 (pixel 1) of flags[y / 16]
-  flags[0] = tile::prmt(st0, st1, 0x5410u);
-  flags[1] = tile::prmt(st0, st1, 0x7632u);
+#pragma unroll
+  for (int h = 0; h < Geo<T, K>::NF; ++h) {
+    const uint32_t a = (uint32_t)((uint64_t)st0 >> (32 * (h >> 1))), b = (uint32_t)((uint64_t)st1 >> (32 * (h >> 1)));
+    flags[h] = 16 * h >= ROWS ? 0u : tile::prmt(a, b, (h & 1) ? 0x7632u : 0x5410u);
+  }
 }
 
 // Median of queued pixels (entries y << 8 | x in warp-tile coords), two per lane.
@@ -418,7 +438,10 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
   const bool fnr = p.method == 0;
   // pass q writes out when (P-1-q) is even, else tmp (the last pass lands in out)
   auto dst_is_out = [&](int q) { return !MP || ((p.passes - 1 - q) & 1) == 0; };
-  auto tile_at = [&](int t) { return MP ? tile_of_mp(p, t, tiles_per_frame) : tile_of(p, t, tiles_per_frame); };
+  constexpr int TH = G::TH, NF = G::NF;
+  auto tile_at = [&](int t) {
+    return MP ? tile_of_mp<TH>(p, t, tiles_per_frame) : tile_of<TH>(p, t, tiles_per_frame);
+  };
   uint32_t replaced = 0, detected = 0;
   bool pred_dense = false;  // k = 5 / 7 FNR: this warp's last tile took the dense stage
 
@@ -441,7 +464,7 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
       const CUtensorMap* src = map0;
       if (MP && ti.pass > 0) {
         // wait for the pass-(q-1) tiles under this tile's box, then read their output
-        const int tx = ti.x0 / WW, ty = (ti.y0 - p.row_begin) / WH;
+        const int tx = ti.x0 / WW, ty = (ti.y0 - p.row_begin) / TH;
         const unsigned int* fl = p.flags + 32 + (size_t)(ti.pass - 1) * npass + (size_t)ti.b * tiles_per_frame;
         // the (up to) 9 flags with independent relaxed loads, one fence once all match
         // (chained acquire loads would serialise nine L2 round trips per tile)
@@ -549,38 +572,41 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
                                                  true, true, none, true, p.one, &det_t);
         detected += det_t;
         n = (int)__reduce_add_sync(0xffffffffu, det_t);
-        pred_dense = n * WH > p.dense_min * ti.rows;
+        pred_dense = n * TH > p.dense_min * ti.rows;
       }
     }
     if (fused) {
     } else if (fnr) {
-      uint32_t flags[2];
+      uint32_t flags[NF];
       T* outp = out_tile + 2 * lane;
-      if (valid_w == WW && valid_h == WH) {
-        if constexpr (K >= IRDN_ROLLED_MIN_K) detect_rolled<T, K, true>(s_in, c0, outp, p.out_pitch, WH, true, true, flags, p.one);
-        else detect<T, K, true>(s_in, c0, outp, p.out_pitch, WH, true, true, flags, p.one);
-      } else if (WH == 32 && valid_w == WW && valid_h == WH / 2 && ti.rows == WH / 2) {
+      if (valid_w == WW && valid_h == TH) {
+        if constexpr (K >= IRDN_ROLLED_MIN_K) detect_rolled<T, K, true>(s_in, c0, outp, p.out_pitch, TH, true, true, flags, p.one);
+        else detect<T, K, true>(s_in, c0, outp, p.out_pitch, TH, true, true, flags, p.one);
+      } else if (TH % 32 == 0 && valid_w == WW && valid_h == TH / 2 && ti.rows == TH / 2) {
         if constexpr (K >= IRDN_ROLLED_MIN_K)
-          detect_rolled<T, K, true, WH / 2>(s_in, c0, outp, p.out_pitch, WH / 2, true, true, flags, p.one);
-        else detect<T, K, true, WH / 2>(s_in, c0, outp, p.out_pitch, WH / 2, true, true, flags, p.one);
-        flags[1] = 0u;
+          detect_rolled<T, K, true, TH / 2>(s_in, c0, outp, p.out_pitch, TH / 2, true, true, flags, p.one);
+        else detect<T, K, true, TH / 2>(s_in, c0, outp, p.out_pitch, TH / 2, true, true, flags, p.one);
+#pragma unroll
+        for (int h = TH / 32; h < NF; ++h) flags[h] = 0u;
       } else {
         if constexpr (K >= IRDN_ROLLED_MIN_K)
           detect_rolled<T, K, false>(s_in, c0, outp, p.out_pitch, valid_h, ok0, ok1, flags, p.one);
         else detect<T, K, false>(s_in, c0, outp, p.out_pitch, valid_h, ok0, ok1, flags, p.one);
         const uint32_t colm = (ok0 ? 0xFFFFu : 0u) | (ok1 ? 0xFFFF0000u : 0u);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < NF; ++h) {
           const int v = min(16, max(0, valid_h - 16 * h));
           const uint32_t rowm = v >= 16 ? 0xFFFFu : ((1u << v) - 1u);
           flags[h] &= colm & (rowm | (rowm << 16));
         }
       }
-      if (WH == 16) flags[1] = 0u;
+      if (TH == 16 && NF > 1) flags[NF - 1] = 0u;
 #ifdef IRDN_TIMELINE
       IRDN_TL_NOW(t_det);
 #endif
-      const int cnt = __popc(flags[0]) + __popc(flags[1]);
+      int cnt = 0;
+#pragma unroll
+      for (int h = 0; h < NF; ++h) cnt += __popc(flags[h]);
       int incl = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -594,7 +620,7 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
       bool dense = false;
       if constexpr (kDense<K>) {
         // many flagged pixels: every pixel's median from shared sorted rows (fnr_dense.cuh)
-        if (p.dense_min >= 0 && n * WH > p.dense_min * ti.rows) {  // dense_min: per full-height tile
+        if (p.dense_min >= 0 && n * TH > p.dense_min * ti.rows) {  // dense_min: per full-height tile
           dense = true;
           replaced += dense_tile<T, K, BOXW>(s_in, c0, out_tile + 2 * lane, p.out_pitch, ti.rows, valid_h, ok0,
                                              ok1, flags, true, p.one);
@@ -605,12 +631,12 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
         if (off < q0 + QCAP && off + cnt > q0) {
           int idx = off - q0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < NF; ++h) {
             uint32_t f = flags[h];
             while (f) {
               const int bit = __ffs(f) - 1;
               f &= f - 1u;
-              if (QCAP >= WW * WH || (unsigned)idx < (unsigned)QCAP)
+              if (QCAP >= WW * TH || (unsigned)idx < (unsigned)QCAP)
                 s_q[idx] = (uint16_t)(ebase + ((uint32_t)(16 * h + (bit & 15)) << 8) + (uint32_t)(bit >> 4));
               ++idx;
             }
@@ -657,7 +683,7 @@ __device__ __forceinline__ void warp_body(const CUtensorMap* map0, const CUtenso
       __threadfence();
       __syncwarp();
       if (lane == 0) {
-        const int tx = ti.x0 / WW, ty = (ti.y0 - p.row_begin) / WH;
+        const int tx = ti.x0 / WW, ty = (ti.y0 - p.row_begin) / TH;
         unsigned int* f =
             p.flags + 32 + (size_t)ti.pass * npass + (size_t)ti.b * tiles_per_frame + ty * p.tiles_x + tx;
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");

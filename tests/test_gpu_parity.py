@@ -345,7 +345,7 @@ def test_host_entry_pinned_and_pageable_buffers(cuda_ok, in_pinned, out_pinned):
 def test_randomized_shapes_windows_methods(cuda_ok):
     """Seeded fuzz: random batch / shape / window / dtype / method / passes / value
     distribution (incl. low-entropy images with many ties), GPU vs oracle, bit-exact pixels
-    and counters. Shapes straddle the tile sizes (64x32 warp tiles, 128-wide 3x3 tiles,
+    and counters. Shapes straddle the tile sizes (64x32 warp tiles, 64x48 for k = 11, 128-wide 3x3 tiles,
     16-byte alignment of rows) so partial tiles, generic fallbacks and edge fix-ups all run."""
     rng = np.random.default_rng(20261020)
     for case in range(60):
@@ -368,6 +368,28 @@ def test_randomized_shapes_windows_methods(cuda_ok):
         got, gst = gpu_filter(img, k, method, passes)
         assert np.array_equal(got, want), (case, dtype, k, img.shape, method, passes)
         assert gst == wst, (case, gst, wst)
+
+
+def test_tall_tiles_11x11(cuda_ok):
+    """k = 11 runs 64 x 48 warp tiles (fnr_warp.cuh WHK): heights on both sides of one, two
+    and three tile rows, whole and partial tile columns, sparse impulses (one queue round per
+    tile) and dense ones (several rounds), FNR / MF, passes 1-2, u8 / u16."""
+    rng = np.random.default_rng(1148)
+    for case, (h, w) in enumerate([(48, 64), (47, 128), (49, 70), (96, 64), (97, 200), (95, 192), (144, 64),
+                                   (150, 130), (24, 64), (1, 64), (11, 300)]):
+        dtype = np.uint16 if case % 2 == 0 else np.uint8
+        top = 16384 if dtype == np.uint16 else 256
+        yy, xx = np.mgrid[0:h, 0:w]
+        img = ((yy * 5 + xx * 3) % (top - 7)).astype(dtype)[None].repeat(2, axis=0).copy()
+        m = rng.random(img.shape) < (0.02 if case % 3 else 0.35)
+        img[m] = rng.integers(0, top, int(m.sum())).astype(dtype)
+        for method, passes in (("fnr", 1), ("fnr", 2), ("mf", 1)):
+            if method == "mf" and h * w > 64 * 64:
+                continue  # the 121-input network on every pixel: keep the case small
+            want, wst = _oracle(img, 11, method, passes)
+            got, gst = gpu_filter(img, 11, method, passes)
+            assert np.array_equal(got, want), (h, w, dtype, method, passes)
+            assert gst == wst, (h, w, method, passes, gst, wst)
 
 
 def test_fnr_pass_mf_pass_accumulate_like_the_reference(cuda_ok):
