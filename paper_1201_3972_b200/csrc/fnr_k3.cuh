@@ -26,10 +26,11 @@
 //                  noisy lane and 0 otherwise; out = c + (med - c) s
 //   counters       detected += s, replaced += sat(|med - c| s), f16x2 accumulators
 //                  flushed to integers once per tile
-//   MF             out = med
 // The min/max network and the key shuffles issue on the ALU pipe, the f16x2 select and
 // counters and the sums on the FMA pipe (measured half-rate each, dual-issuing:
 // profiles/pipe_probe_r02.txt).
+// MF (every pixel replaced, no detector, select or counters) takes the row-first body
+// below: its work is almost all on the ALU pipe, where that layout needs fewer shuffles.
 #pragma once
 #include <cuda_fp16.h>
 #include <type_traits>
@@ -144,6 +145,50 @@ __device__ __forceinline__ void make_keys(const RowSeg& t, const RowSeg& b, uint
   k[COLS + 1] = tile::prmt(tile::prmt(t.r, b.r, 0x4400u), KEY_BYTE, 0x4240u);
 }
 
+// ---- Row-first layout (MF) ---------------------------------------------------------
+// A word holds two pixels of ONE row two columns apart (the even or the odd bytes of an
+// input word, zero-extended in place), so the three rows of a window are three registers
+// and only the raw input needs shifted copies. A thread owns 8 columns x RB rows:
+//   widen      per row and input word w = (c0 c1 c2 c3): E = (c0, c2), O = (c1, c3),
+//              L = (c-1, c1) from the previous O, R = (c2, c4) from the next E: 4 PRMT / 4 px
+//   row sort   outputs (c0, c2): sort3(L, E, O); outputs (c1, c3): sort3(E, O, R):
+//              lo = min3, hi = max3, mid = sum - lo - hi (IMADs), once per input row
+//   vertical   for output rows y, y+1 from sorted rows y-1 .. y+2 (registers):
+//              max3(lo), min3(hi), med3(mid) with the sorted middle pair (rows y, y+1) shared
+//              between the two output rows, then the final median of the three.
+// Against the column-first body: 1.0 instead of 1.9 PRMT per pixel and no column halo
+// (18 / 16) for a row halo of (RB + 2) / RB: 6.0 instead of 8.1 ALU-pipe instructions per
+// pixel. MF c5 0.622 -> 0.541 ms (0.72 of the HBM roofline). For FNR the same layout needs
+// 72 registers (the centre words ride along) and measured within 1 % of the column-first
+// body, so FNR keeps that one.
+namespace rows {
+constexpr int RCOLS = 8;                 // output columns per thread
+constexpr int RTPR = TW / RCOLS;         // 16 threads per row band
+constexpr int RBANDS = THREADS / RTPR;   // 8 row bands per tile
+struct Sorted {
+  uint32_t lo[4], mid[4], hi[4];         // words: columns (0,2), (1,3), (4,6), (5,7)
+};
+// Sorted horizontal triples of one input row; p = the thread's first column in that row.
+__device__ __forceinline__ void sort_row(const uint8_t* p, Sorted& s, uint32_t one, uint32_t m1) {
+  const uint2 m = *reinterpret_cast<const uint2*>(p);
+  const uint32_t l = *reinterpret_cast<const uint32_t*>(p - 4);
+  const uint32_t r = *reinterpret_cast<const uint32_t*>(p + 8);
+  const uint32_t E0 = tile::prmt(m.x, 0u, 0x4240u), O0 = tile::prmt(m.x, 0u, 0x4341u);
+  const uint32_t E1 = tile::prmt(m.y, 0u, 0x4240u), O1 = tile::prmt(m.y, 0u, 0x4341u);
+  const uint32_t L0 = tile::prmt(l, O0, 0x5453u);   // (c-1, c1)
+  const uint32_t L1 = tile::prmt(O0, O1, 0x5432u);  // (c3, c5)
+  const uint32_t R0 = tile::prmt(E0, E1, 0x5432u);  // (c2, c4)
+  const uint32_t R1 = tile::prmt(E1, r, 0x3432u);   // (c6, c8)
+  const uint32_t a[4] = {L0, E0, L1, E1}, b[4] = {E0, O0, E1, O1}, c[4] = {O0, R0, O1, R1};
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    s.lo[w] = vmin3(a[w], b[w], c[w]);
+    s.hi[w] = vmax3(a[w], b[w], c[w]);
+    s.mid[w] = fma_sub(fma_sub(fma_add(c[w], one, fma_add(a[w], one, b[w])), m1, s.lo[w]), m1, s.hi[w]);
+  }
+}
+}  // namespace rows
+
 // Replicate-edge fix-up of the box cells outside the frame (TMA zero-fills them).
 template <int BAND>
 __device__ __forceinline__ void fix_edges(uint8_t* s_in, int gx_lo, int gy_lo, int width, int height) {
@@ -235,9 +280,11 @@ __global__ void __launch_bounds__(THREADS, FULL ? IRDN_K3_MINBLOCKS : 5) fnr_k3_
   }
   __syncthreads();
 
-  const int tc = tid % TPR, band = tid / TPR;
-  const int x0 = tc * COLS;   // first tile column of this thread
-  const int y0 = band * BAND;  // first tile row of this thread
+  // FNR: column-first body, 16 columns x BAND rows per thread; MF: row-first, 8 columns x 2 BAND rows
+  constexpr int RB = FNR ? BAND : G::TH / rows::RBANDS;
+  const int tc = FNR ? tid % TPR : tid % rows::RTPR, band = FNR ? tid / TPR : tid / rows::RTPR;
+  const int x0 = tc * (FNR ? COLS : rows::RCOLS);  // first tile column of this thread
+  const int y0 = band * RB;                        // first tile row of this thread
   uint8_t* const out_base = reinterpret_cast<uint8_t*>(p.out);
 
   for (int iter = 0;; ++iter) {
@@ -252,7 +299,72 @@ __global__ void __launch_bounds__(THREADS, FULL ? IRDN_K3_MINBLOCKS : 5) fnr_k3_
       __syncthreads();
     }
     uint32_t dacc = 0, racc = 0;  // f16x2 counters of this tile
-    auto body = [&](auto masked) {
+    // MF: row-first body (header of namespace rows)
+    auto body_mf = [&](auto masked) {
+      constexpr bool MASKED = decltype(masked)::value;
+      int valid_w = TW, valid_h = G::TH;
+      if constexpr (MASKED) {
+        valid_w = min(TW, p.width - ti.tx0);
+        valid_h = min(G::TH, p.row_end - ti.ty0);
+      }
+      uint8_t* outp = out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.ty0 - p.row_begin + y0) * p.out_pitch +
+                      ti.tx0 + x0;
+      // smem row of tile row y is y + 1; the thread's segment starts at box column R + x0
+      const uint8_t* srow = s_in + y0 * G::BOXW + G::R + x0;
+      rows::Sorted ring[4];
+      rows::sort_row(srow, ring[0], one, m1);
+      rows::sort_row(srow + G::BOXW, ring[1], one, m1);
+      // one output row from the sorted rows u (above), v, w (below); pm / qm = the sorted pair
+      // of the two middle rows this step's output rows share, t = the third row's middles
+      auto out_row = [&](const rows::Sorted& u, const rows::Sorted& v, const rows::Sorted& w, const uint32_t (&pm)[4],
+                         const uint32_t (&qm)[4], const uint32_t (&t)[4], int yr) {
+        uint32_t out[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t md = vmax2(pm[i], vmin2(qm[i], t[i]));
+          const uint32_t mxlo = vmax3(u.lo[i], v.lo[i], w.lo[i]);
+          const uint32_t mnhi = vmin3(u.hi[i], v.hi[i], w.hi[i]);
+          const uint32_t mn3 = vmin3(mxlo, md, mnhi), mx3 = vmax3(mxlo, md, mnhi);
+          out[i] = fma_sub(fma_sub(fma_add(mnhi, one, fma_add(mxlo, one, md)), m1, mn3), m1, mx3);
+        }
+        // (c0, c2) and (c1, c3) interleave to one output word
+        const uint32_t w0 = tile::prmt(out[0], out[1], 0x6240u), w1 = tile::prmt(out[2], out[3], 0x6240u);
+        uint8_t* const orow = outp;
+        outp += p.out_pitch;
+        if constexpr (!MASKED) {
+          *reinterpret_cast<uint2*>(orow) = make_uint2(w0, w1);
+        } else if (yr < valid_h) {
+          if (x0 + rows::RCOLS <= valid_w) {
+            *reinterpret_cast<uint2*>(orow) = make_uint2(w0, w1);
+          } else {
+#pragma unroll
+            for (int i = 0; i < rows::RCOLS; ++i)
+              if (x0 + i < valid_w) orow[i] = (uint8_t)((i < 4 ? w0 : w1) >> (8 * (i & 3)));
+          }
+        }
+      };
+      // output rows 2s, 2s + 1 of the thread: r0, r1 = sorted rows above / at 2s (carried), r2, r3 new
+      auto step = [&](int s, rows::Sorted& r0, rows::Sorted& r1, rows::Sorted& r2, rows::Sorted& r3) {
+        rows::sort_row(srow + (2 * s + 2) * G::BOXW, r2, one, m1);
+        uint32_t pm[4], qm[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          pm[i] = vmin2(r1.mid[i], r2.mid[i]);
+          qm[i] = vmax2(r1.mid[i], r2.mid[i]);
+        }
+        out_row(r0, r1, r2, pm, qm, r0.mid, y0 + 2 * s);
+        rows::sort_row(srow + (2 * s + 3) * G::BOXW, r3, one, m1);
+        out_row(r1, r2, r3, pm, qm, r3.mid, y0 + 2 * s + 1);
+      };
+      // two steps per iteration: the ring's roles swap without register moves
+#pragma unroll 1
+      for (int s = 0; s < RB / 2; s += 2) {
+        step(s, ring[0], ring[1], ring[2], ring[3]);
+        step(s + 1, ring[2], ring[3], ring[0], ring[1]);
+      }
+    };
+    // FNR: column-first body (header of this file)
+    auto body_fnr = [&](auto masked) {
       constexpr bool MASKED = decltype(masked)::value;
       int valid_w = TW, valid_h = G::TH;
       if constexpr (MASKED) {
@@ -316,21 +428,17 @@ __global__ void __launch_bounds__(THREADS, FULL ? IRDN_K3_MINBLOCKS : 5) fnr_k3_
               med = fma_sub(fma_sub(fma_add(mnhi, one, fma_add(mxlo, one, md)), m1, mn3), m1, mx3);
             else
               med = mxlo + md + mnhi - mn3 - mx3;
-            if constexpr (FNR) {
-              const uint32_t c = S[o + 1];
-              const uint32_t mn = vmin3(lo[o], lo[o + 1], lo[o + 2]), mx = vmax3(hi[o], hi[o + 1], hi[o + 2]);
-              uint32_t sflag = hfma_sat(hsub(mn, c), hsub(mx, c), F16_ONE);  // 1.0: noisy lane
-              const uint32_t dm = hsub(med, c);
-              out[o] = hfma(dm, sflag, c);
-              if constexpr (MASKED) {
-                const bool colok = x0 + o < valid_w;
-                sflag &= colok ? rowmask : 0u;
-              }
-              racc = hadd(racc, hmul_sat_abs(dm, sflag));
-              dacc = hadd(dacc, sflag);
-            } else {
-              out[o] = med;
+            const uint32_t c = S[o + 1];
+            const uint32_t mn = vmin3(lo[o], lo[o + 1], lo[o + 2]), mx = vmax3(hi[o], hi[o + 1], hi[o + 2]);
+            uint32_t sflag = hfma_sat(hsub(mn, c), hsub(mx, c), F16_ONE);  // 1.0: noisy lane
+            const uint32_t dm = hsub(med, c);
+            out[o] = hfma(dm, sflag, c);
+            if constexpr (MASKED) {
+              const bool colok = x0 + o < valid_w;
+              sflag &= colok ? rowmask : 0u;
             }
+            racc = hadd(racc, hmul_sat_abs(dm, sflag));
+            dacc = hadd(dacc, sflag);
           }
         }
         // keys -> bytes: byte 0 of a key is the upper row's pixel, byte 2 the lower row's
@@ -366,8 +474,12 @@ __global__ void __launch_bounds__(THREADS, FULL ? IRDN_K3_MINBLOCKS : 5) fnr_k3_
         outp += 2 * p.out_pitch;
       }
     };
-    if (FULL || (ti.tx0 + TW <= p.width && ti.ty0 + G::TH <= p.row_end)) body(std::false_type{});
-    else if constexpr (!FULL) body(std::true_type{});
+    auto run = [&](auto& body) {
+      if (FULL || (ti.tx0 + TW <= p.width && ti.ty0 + G::TH <= p.row_end)) body(std::false_type{});
+      else if constexpr (!FULL) body(std::true_type{});
+    };
+    if constexpr (FNR) run(body_fnr);
+    else run(body_mf);
     if constexpr (FNR) {
       det_total += hsum_lanes(dacc);
       rep_total += hsum_lanes(racc);
