@@ -143,11 +143,10 @@ def job_pixels(cfg, world: int) -> int:
 # ---------------------------------------------------------------------------
 # Packed min/max instructions (VIMNMX / VIMNMX3 .U16x2, two pixels each) per two output
 # pixels, from the kernels' static schedule:
-#   dense 3x3 FNR (fnr_k3.cuh, 16 output columns + 2 halo columns per thread):
-#     column sort 2 x 18/16, window min/max of column lows/highs 4, median of the three
-#     column middles 3 (sorted shared pair + clamp), final median-of-3 2
-#   dense 3x3 MF (row-first body, 20 output rows + 2 halo rows per thread in 160-row tiles):
-#     row sort 2 x 22/20, max of lows / min of highs 2, middles 3, final median-of-3 2
+#   dense 3x3 (fnr_k3.cuh, row-first; 160-row tiles: FNR 40 output rows + 2 halo rows per
+#     thread, MF 20 + 2): row sort 2 x (rows + 2) / rows, max of lows / min of highs 2, median
+#     of the three row middles 3 (sorted shared pair + clamp), final median-of-3 2, FNR: window
+#     min / max for the detector 2
 #   warp kernel k = 5..11 (fnr_warp.cuh, 64 x 32 tiles, 64 x 48 for k = 11, pixel pairs): detector
 #     (K-1)(1 + 2r/rows) horizontal + (K-1) vertical + 1 flag test per pair, plus the median
 #     network for two flagged pixels (select_nets.cuh) times the detected fraction.
@@ -164,12 +163,11 @@ FUSED_DET_PER_PAIR = {5: 6.0, 7: 5.5}
 
 def static_ops(cfg, detected_fraction: float, method: str = "fnr") -> dict:
     if cfg.k == 3 and cfg.dtype == "u8":
-        if method == "mf":  # row-first body: row sort 2 x 22/20 (160-row tiles), max3 lo, min3 hi, middles 3, final 2
-            per_pair = 2 * 22 / 20 + 2 + 3 + 2
-        else:
-            per_pair = 2 * 18 / 16 + 4 + 3 + 2
+        # row sort 2 x (rows + 2) / rows per thread (160-row tiles: MF 20 rows, FNR 40), max3 lo,
+        # min3 hi, middles 3, final 2, FNR: + min3 lo / max3 hi for the detector
+        per_pair = (2 * 22 / 20 + 2 + 3 + 2) if method == "mf" else (2 * 42 / 40 + 2 + 3 + 2 + 2)
         return {"method": ("dense sorted-rows 3x3 median" if method == "mf" else
-                           "dense sorted-columns 3x3 median + extremum detector") + " (every pixel)",
+                           "dense sorted-rows 3x3 median + extremum detector") + " (every pixel)",
                 "minmax_instr_per_px": round(per_pair / 2, 3),
                 "minmax_lane_ops_per_px": round(per_pair, 3),
                 "note": "VIMNMX(3).U16x2 instructions per pixel (each covers 2 pixels); lane ops per pixel"}

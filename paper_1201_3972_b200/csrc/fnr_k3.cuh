@@ -4,33 +4,35 @@
 // no queue: detector, median, select and counters run branch-free on packed words and
 // the result goes straight to HBM (reference filters.py:156-180).
 //
-// Keys. One 32-bit word holds one column's pixels of two consecutive rows, each as the
-// 16-bit key 0x6400 | v: as an unsigned integer it is monotone in v (so VIMNMX.U16x2
-// min / max / median on keys are min / max / median on pixels), and as an fp16 number it
-// is exactly 1024 + v (so differences of keys are exact small integers in f16x2
-// arithmetic). A word's lane 0 is the upper row. Keys are built from two row words with
-// two PRMTs per pair of columns plus one per column (interleave the rows, then insert
-// the 0x64 exponent byte).
-//
-// Per step (two output rows y, y+1; A = keys of rows y-1,y; B = rows y+1,y+2;
-// S = rows y,y+1 = one PRMT of A and B), for each of COLS + 2 columns:
-//   column sort    lo = min3(A,S,B), hi = max3(A,S,B), mid = A+S+B-lo-hi   (lanewise the
-//                  sorted 3-row column of both output rows; the integer sum is exact in 32
-//                  bits because every lane of the result is in range)
-// and for each output column (columns j-1, j, j+1):
-//   median of 9    med3(max3(lo), med3(mid), min3(hi))  (the sorted-columns identity);
-//                  med3(mid) shares the sorted middle pair between horizontal neighbours:
-//                  p,q = sort(mid[j], mid[j+1]) serves outputs j-1 and j as clamp(., p, q)
+// Layout (row-first). One 32-bit word holds two pixels of ONE row two columns apart: the
+// even or the odd bytes of an input word, widened in place, so the three rows of a window
+// are three registers and only the raw input needs shifted copies. FNR widens each pixel to
+// the 16-bit key 0x6400 | v: as an unsigned integer it is monotone in v (VIMNMX.U16x2 min /
+// max / median on keys are those of the pixels), and as an fp16 number it is exactly
+// 1024 + v (differences of keys are exact small integers in f16x2 arithmetic). MF
+// zero-extends. A thread owns NW output words (FNR: 2 = one input word = 4 columns, MF: 4 =
+// 8 columns) and walks RB rows down its tile:
+//   widen      per row and input word (c0 c1 c2 c3): E = (c0, c2), O = (c1, c3), L = (c-1, c1)
+//              from the previous O, R = (c2, c4) from the next E: 4 PRMT per 4 pixels
+//   row sort   outputs (c0, c2): sort3(L, E, O); outputs (c1, c3): sort3(E, O, R): lo = min3,
+//              hi = max3, mid = sum - lo - hi (IMADs: the integer sum is exact in 32 bits
+//              because every lane of the result is in range), once per input row
+//   vertical   output rows y, y+1 per step from the sorted rows y-1 .. y+2 (a ring of four in
+//              registers; two steps per loop iteration so the roles swap without moves):
+//   median of 9    med3(max3(lo), med3(mid), min3(hi))  (the sorted-rows identity); med3(mid)
+//                  shares the sorted middle pair p, q = sort(mid[y], mid[y+1]) between the
+//                  step's two output rows as clamp(., p, q)
 //   detector       min9 = min3(lo), max9 = max3(hi); noisy iff c == min9 or c == max9
 //   select (FNR)   in f16x2 on the FMA pipe: s = sat(1 + (min9 - c)(max9 - c)) is 1.0 for a
 //                  noisy lane and 0 otherwise; out = c + (med - c) s
 //   counters       detected += s, replaced += sat(|med - c| s), f16x2 accumulators
 //                  flushed to integers once per tile
-// The min/max network and the key shuffles issue on the ALU pipe, the f16x2 select and
+//   MF             out = med (no detector, select or counters)
+// The min/max network and the byte shuffles issue on the ALU pipe, the f16x2 select and
 // counters and the sums on the FMA pipe (measured half-rate each, dual-issuing:
-// profiles/pipe_probe_r02.txt).
-// MF (every pixel replaced, no detector, select or counters) takes the row-first body
-// below: its work is almost all on the ALU pipe, where that layout needs fewer shuffles.
+// profiles/pipe_probe_r02.txt). Round 2 measured this layout against a column-first one
+// (one word = one column's pixels of two consecutive rows, 16 columns per thread): FNR
+// 0.754 vs 0.770 ms and MF 0.539 vs 0.622 ms on c5.
 #pragma once
 #include <cuda_fp16.h>
 #include <type_traits>
@@ -40,33 +42,24 @@ namespace irdn {
 namespace k3 {
 
 constexpr int THREADS = 128;
-constexpr int COLS = 16;                // output columns per thread (one 16-byte row segment)
-constexpr int TPR = 8;                  // threads per row band
-constexpr int TW = COLS * TPR;          // tile width: 128 pixels
-constexpr int BANDS = THREADS / TPR;    // 16 row bands per tile
+constexpr int TW = 128;                 // tile width in pixels
+constexpr int BANDS = 16;               // tile height unit: TH = BANDS * BAND rows
 #ifndef IRDN_K3_NSTAGE
 #define IRDN_K3_NSTAGE 1  // measured: 1 stage x 8 CTAs/SM beats 2 stages x 4 (c5 0.789 vs 0.797 ms)
 #endif
 constexpr int NSTAGE = IRDN_K3_NSTAGE;
 
 // Pipe placement of the integer helper arithmetic (A/B switches; the defaults are the
-// measured best): the row-pair shift S and the column middle on the FMA pipe (IMADs), the
-// final median-of-3 sum on the ALU pipe (IADD3).
-#ifndef IRDN_K3_S_FMA
-#define IRDN_K3_S_FMA 0
-#endif
+// measured best for FNR, profiles/r02/k3_rows/ab_5_fnr4.txt): the row-sort middle on the FMA
+// pipe (IMADs), the final median-of-3 sum on the ALU pipe (IADD3). MF puts both on the FMA pipe.
 #ifndef IRDN_K3_MID_FMA
 #define IRDN_K3_MID_FMA 1
-#endif
-#ifndef IRDN_K3_UNROLL
-#define IRDN_K3_UNROLL 1
 #endif
 #ifndef IRDN_K3_FIN_FMA
 #define IRDN_K3_FIN_FMA 0
 #endif
-constexpr int kStepUnroll = IRDN_K3_UNROLL;
 
-// Tile height TH = BANDS * BAND (BAND = rows per thread, even): 160 (BAND 10), 128, 64 or 32.
+// Tile height TH = BANDS * BAND (BAND even): 160 (BAND 10), 128, 96, 64 or 32.
 template <int BAND>
 struct Geo {
   static_assert(BAND % 2 == 0, "two output rows per step");
@@ -118,76 +111,60 @@ __device__ __forceinline__ uint32_t hsum_lanes(uint32_t h) {
 constexpr uint32_t KEY_BYTE = 0x64646464u;  // f16 exponent byte of 1024 + v
 constexpr uint32_t F16_ONE = 0x3C003C00u;
 
-// A row segment of one thread: 16 pixels at tile columns x0 .. x0+15 plus the words
-// holding columns x0-1 (byte 3 of `l`) and x0+16 (byte 0 of `r`).
-struct RowSeg {
-  uint4 m;
-  uint32_t l, r;
-};
-__device__ __forceinline__ void load_seg(const uint8_t* p, RowSeg& s) {
-  s.m = *reinterpret_cast<const uint4*>(p);
-  s.l = *reinterpret_cast<const uint32_t*>(p - 4);
-  s.r = *reinterpret_cast<const uint32_t*>(p + 16);
-}
-// Keys of columns x0-1 .. x0+16 (k[0] .. k[COLS+1]) for rows (t, b): lane 0 = row t.
-__device__ __forceinline__ void make_keys(const RowSeg& t, const RowSeg& b, uint32_t (&k)[COLS + 2]) {
-  k[0] = tile::prmt(tile::prmt(t.l, b.l, 0x7733u), KEY_BYTE, 0x4240u);  // (t3, t3, b3, b3) -> (t3, 64, b3, 64)
-  const uint32_t tw[4] = {t.m.x, t.m.y, t.m.z, t.m.w}, bw[4] = {b.m.x, b.m.y, b.m.z, b.m.w};
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    const uint32_t i0 = tile::prmt(tw[w], bw[w], 0x5140u);  // (t0, b0, t1, b1)
-    const uint32_t i1 = tile::prmt(tw[w], bw[w], 0x7362u);  // (t2, b2, t3, b3)
-    k[1 + 4 * w] = tile::prmt(i0, KEY_BYTE, 0x4140u);
-    k[2 + 4 * w] = tile::prmt(i0, KEY_BYTE, 0x4342u);
-    k[3 + 4 * w] = tile::prmt(i1, KEY_BYTE, 0x4140u);
-    k[4 + 4 * w] = tile::prmt(i1, KEY_BYTE, 0x4342u);
-  }
-  k[COLS + 1] = tile::prmt(tile::prmt(t.r, b.r, 0x4400u), KEY_BYTE, 0x4240u);
-}
+// Words per thread and row: FNR 2 (4 columns: 56 registers, 8 CTAs per SM; with 4 words the
+// carried centre words push it to 72 registers and 7 CTAs), MF 4 (8 columns, 60 registers).
+template <bool FNR>
+constexpr int kWords = FNR ? 2 : 4;
 
-// ---- Row-first layout (MF) ---------------------------------------------------------
-// A word holds two pixels of ONE row two columns apart (the even or the odd bytes of an
-// input word, zero-extended in place), so the three rows of a window are three registers
-// and only the raw input needs shifted copies. A thread owns 8 columns x RB rows:
-//   widen      per row and input word w = (c0 c1 c2 c3): E = (c0, c2), O = (c1, c3),
-//              L = (c-1, c1) from the previous O, R = (c2, c4) from the next E: 4 PRMT / 4 px
-//   row sort   outputs (c0, c2): sort3(L, E, O); outputs (c1, c3): sort3(E, O, R):
-//              lo = min3, hi = max3, mid = sum - lo - hi (IMADs), once per input row
-//   vertical   for output rows y, y+1 from sorted rows y-1 .. y+2 (registers):
-//              max3(lo), min3(hi), med3(mid) with the sorted middle pair (rows y, y+1) shared
-//              between the two output rows, then the final median of the three.
-// Against the column-first body: 1.0 instead of 1.9 PRMT per pixel and no column halo
-// (18 / 16) for a row halo of (RB + 2) / RB: 6.0 instead of 8.1 ALU-pipe instructions per
-// pixel. MF c5 0.622 -> 0.541 ms (0.72 of the HBM roofline). For FNR the same layout needs
-// 72 registers (the centre words ride along) and measured within 1 % of the column-first
-// body, so FNR keeps that one.
-namespace rows {
-constexpr int RCOLS = 8;                 // output columns per thread
-constexpr int RTPR = TW / RCOLS;         // 16 threads per row band
-constexpr int RBANDS = THREADS / RTPR;   // 8 row bands per tile
+// The sorted horizontal triples of one input row for the thread's NW output words — word 2i:
+// columns (4i, 4i+2), word 2i+1: columns (4i+1, 4i+3) — and the row's own pixels (centres).
+template <int NW>
 struct Sorted {
-  uint32_t lo[4], mid[4], hi[4];         // words: columns (0,2), (1,3), (4,6), (5,7)
+  uint32_t lo[NW], mid[NW], hi[NW], c[NW];
 };
-// Sorted horizontal triples of one input row; p = the thread's first column in that row.
-__device__ __forceinline__ void sort_row(const uint8_t* p, Sorted& s, uint32_t one, uint32_t m1) {
-  const uint2 m = *reinterpret_cast<const uint2*>(p);
-  const uint32_t l = *reinterpret_cast<const uint32_t*>(p - 4);
-  const uint32_t r = *reinterpret_cast<const uint32_t*>(p + 8);
-  const uint32_t E0 = tile::prmt(m.x, 0u, 0x4240u), O0 = tile::prmt(m.x, 0u, 0x4341u);
-  const uint32_t E1 = tile::prmt(m.y, 0u, 0x4240u), O1 = tile::prmt(m.y, 0u, 0x4341u);
-  const uint32_t L0 = tile::prmt(l, O0, 0x5453u);   // (c-1, c1)
-  const uint32_t L1 = tile::prmt(O0, O1, 0x5432u);  // (c3, c5)
-  const uint32_t R0 = tile::prmt(E0, E1, 0x5432u);  // (c2, c4)
-  const uint32_t R1 = tile::prmt(E1, r, 0x3432u);   // (c6, c8)
-  const uint32_t a[4] = {L0, E0, L1, E1}, b[4] = {E0, O0, E1, O1}, c[4] = {O0, R0, O1, R1};
+// p = the thread's first column in that smem row; hi_byte = the byte widened pixels carry
+// above them (KEY_BYTE for FNR, 0 for MF).
+template <int NW, bool FMA_SUM>
+__device__ __forceinline__ void sort_row(const uint8_t* p, Sorted<NW>& s, uint32_t hi_byte, uint32_t one,
+                                         uint32_t m1) {
+  constexpr int NI = NW / 2;  // input words
+  uint32_t in[NI];
+  if constexpr (NI == 1) {
+    in[0] = *reinterpret_cast<const uint32_t*>(p);
+  } else {
+    static_assert(NI == 2, "one or two input words per thread and row");
+    const uint2 m = *reinterpret_cast<const uint2*>(p);
+    in[0] = m.x;
+    in[1] = m.y;
+  }
+  const uint32_t l = *reinterpret_cast<const uint32_t*>(p - 4);       // byte 3: column -1
+  const uint32_t r = *reinterpret_cast<const uint32_t*>(p + 4 * NI);  // byte 0: column 4 NI
+  uint32_t E[NI], O[NI];
 #pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    s.lo[w] = vmin3(a[w], b[w], c[w]);
-    s.hi[w] = vmax3(a[w], b[w], c[w]);
-    s.mid[w] = fma_sub(fma_sub(fma_add(c[w], one, fma_add(a[w], one, b[w])), m1, s.lo[w]), m1, s.hi[w]);
+  for (int i = 0; i < NI; ++i) {
+    E[i] = tile::prmt(in[i], hi_byte, 0x4240u);  // (c0, c2)
+    O[i] = tile::prmt(in[i], hi_byte, 0x4341u);  // (c1, c3)
+  }
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    // (c-1, c1): the high byte of the widened c-1 is O's own high byte
+    const uint32_t L = i == 0 ? tile::prmt(l, O[0], 0x5453u) : tile::prmt(O[i - 1], O[i], 0x5432u);
+    // (c2, c4)
+    const uint32_t R = i == NI - 1 ? tile::prmt(E[i], r, 0x3432u) : tile::prmt(E[i], E[i + 1], 0x5432u);
+    const uint32_t a[2] = {L, E[i]}, b[2] = {E[i], O[i]}, c[2] = {O[i], R};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int w = 2 * i + h;
+      s.lo[w] = vmin3(a[h], b[h], c[h]);
+      s.hi[w] = vmax3(a[h], b[h], c[h]);
+      if constexpr (FMA_SUM)
+        s.mid[w] = fma_sub(fma_sub(fma_add(c[h], one, fma_add(a[h], one, b[h])), m1, s.lo[w]), m1, s.hi[w]);
+      else
+        s.mid[w] = a[h] + b[h] + c[h] - s.lo[w] - s.hi[w];
+      s.c[w] = b[h];
+    }
   }
 }
-}  // namespace rows
 
 // Replicate-edge fix-up of the box cells outside the frame (TMA zero-fills them).
 template <int BAND>
@@ -249,7 +226,7 @@ __global__ void __launch_bounds__(THREADS, FULL ? IRDN_K3_MINBLOCKS : 5) fnr_k3_
   const int tiles_per_frame = p.tiles_x * p.tiles_y;
   const int ntiles = tiles_per_frame * p.batch;
   uint32_t det_total = 0, rep_total = 0;
-  const uint32_t one = p.one, m1 = 0u - p.one, k65536 = p.one << 16;  // opaque: keeps IMADs on the FMA pipe
+  const uint32_t one = p.one, m1 = 0u - p.one;  // opaque: keeps IMADs on the FMA pipe
 
   // (claiming the next tile's index when a tile starts, to overlap the atomic's round trip,
   // measured 0.5 % slower on c5: 0.7839 vs 0.7831 ms)
@@ -280,11 +257,13 @@ __global__ void __launch_bounds__(THREADS, FULL ? IRDN_K3_MINBLOCKS : 5) fnr_k3_
   }
   __syncthreads();
 
-  // FNR: column-first body, 16 columns x BAND rows per thread; MF: row-first, 8 columns x 2 BAND rows
-  constexpr int RB = FNR ? BAND : G::TH / rows::RBANDS;
-  const int tc = FNR ? tid % TPR : tid % rows::RTPR, band = FNR ? tid / TPR : tid / rows::RTPR;
-  const int x0 = tc * (FNR ? COLS : rows::RCOLS);  // first tile column of this thread
-  const int y0 = band * RB;                        // first tile row of this thread
+  constexpr int NW = kWords<FNR>, NC = 2 * NW;  // words / columns per thread
+  constexpr int TPR = TW / NC;                   // threads per row band
+  constexpr int RB = G::TH / (THREADS / TPR);    // rows per thread (FNR: 4 BAND, MF: 2 BAND)
+  static_assert(RB % 4 == 0, "two steps of two output rows per loop iteration");
+  const int x0 = (tid % TPR) * NC;  // first tile column of this thread
+  const int y0 = (tid / TPR) * RB;  // first tile row of this thread
+  const uint32_t hi_byte = FNR ? KEY_BYTE : 0u;
   uint8_t* const out_base = reinterpret_cast<uint8_t*>(p.out);
 
   for (int iter = 0;; ++iter) {
@@ -299,61 +278,92 @@ __global__ void __launch_bounds__(THREADS, FULL ? IRDN_K3_MINBLOCKS : 5) fnr_k3_
       __syncthreads();
     }
     uint32_t dacc = 0, racc = 0;  // f16x2 counters of this tile
-    // MF: row-first body (header of namespace rows)
-    auto body_mf = [&](auto masked) {
+    auto body = [&](auto masked) {
       constexpr bool MASKED = decltype(masked)::value;
       int valid_w = TW, valid_h = G::TH;
+      uint32_t colmask[NW];  // partial tiles: lanes of columns inside the tile
+#pragma unroll
+      for (int w = 0; w < NW; ++w) colmask[w] = 0xFFFFFFFFu;
       if constexpr (MASKED) {
         valid_w = min(TW, p.width - ti.tx0);
         valid_h = min(G::TH, p.row_end - ti.ty0);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const int cw = x0 + (w & 1) + 4 * (w >> 1);  // columns cw and cw + 2
+          colmask[w] = (cw < valid_w ? 0x0000FFFFu : 0u) | (cw + 2 < valid_w ? 0xFFFF0000u : 0u);
+        }
       }
       uint8_t* outp = out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.ty0 - p.row_begin + y0) * p.out_pitch +
                       ti.tx0 + x0;
       // smem row of tile row y is y + 1; the thread's segment starts at box column R + x0
       const uint8_t* srow = s_in + y0 * G::BOXW + G::R + x0;
-      rows::Sorted ring[4];
-      rows::sort_row(srow, ring[0], one, m1);
-      rows::sort_row(srow + G::BOXW, ring[1], one, m1);
-      // one output row from the sorted rows u (above), v, w (below); pm / qm = the sorted pair
-      // of the two middle rows this step's output rows share, t = the third row's middles
-      auto out_row = [&](const rows::Sorted& u, const rows::Sorted& v, const rows::Sorted& w, const uint32_t (&pm)[4],
-                         const uint32_t (&qm)[4], const uint32_t (&t)[4], int yr) {
-        uint32_t out[4];
+      constexpr bool MID_FMA = !FNR || IRDN_K3_MID_FMA;
+      using Row = Sorted<NW>;
+      Row ring[4];
+      sort_row<NW, MID_FMA>(srow, ring[0], hi_byte, one, m1);
+      sort_row<NW, MID_FMA>(srow + G::BOXW, ring[1], hi_byte, one, m1);
+      // one output row (tile row yr) from the sorted rows u (above), v, w (below); pm / qm = the
+      // sorted pair of the two middle rows this step's output rows share, t = the third middles
+      auto out_row = [&](const Row& u, const Row& v, const Row& w, const uint32_t (&pm)[NW], const uint32_t (&qm)[NW],
+                         const uint32_t (&t)[NW], int yr) {
+        uint32_t out[NW];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < NW; ++i) {
           const uint32_t md = vmax2(pm[i], vmin2(qm[i], t[i]));
           const uint32_t mxlo = vmax3(u.lo[i], v.lo[i], w.lo[i]);
           const uint32_t mnhi = vmin3(u.hi[i], v.hi[i], w.hi[i]);
           const uint32_t mn3 = vmin3(mxlo, md, mnhi), mx3 = vmax3(mxlo, md, mnhi);
-          out[i] = fma_sub(fma_sub(fma_add(mnhi, one, fma_add(mxlo, one, md)), m1, mn3), m1, mx3);
+          uint32_t med;
+          if (!FNR || IRDN_K3_FIN_FMA == 1 || (IRDN_K3_FIN_FMA == 2 && (i & 1)))
+            med = fma_sub(fma_sub(fma_add(mnhi, one, fma_add(mxlo, one, md)), m1, mn3), m1, mx3);
+          else
+            med = mxlo + md + mnhi - mn3 - mx3;
+          if constexpr (FNR) {
+            const uint32_t c = v.c[i];
+            const uint32_t mn = vmin3(u.lo[i], v.lo[i], w.lo[i]), mx = vmax3(u.hi[i], v.hi[i], w.hi[i]);
+            uint32_t sflag = hfma_sat(hsub(mn, c), hsub(mx, c), F16_ONE);  // 1.0: noisy lane
+            const uint32_t dm = hsub(med, c);
+            out[i] = hfma(dm, sflag, c);
+            if constexpr (MASKED) sflag &= yr < valid_h ? colmask[i] : 0u;
+            racc = hadd(racc, hmul_sat_abs(dm, sflag));
+            dacc = hadd(dacc, sflag);
+          } else {
+            out[i] = med;
+          }
         }
-        // (c0, c2) and (c1, c3) interleave to one output word
-        const uint32_t w0 = tile::prmt(out[0], out[1], 0x6240u), w1 = tile::prmt(out[2], out[3], 0x6240u);
+        // widened pixels -> bytes: (c0, c2) and (c1, c3) interleave to one output word
+        uint32_t ow[NW / 2];
+#pragma unroll
+        for (int i = 0; i < NW / 2; ++i) ow[i] = tile::prmt(out[2 * i], out[2 * i + 1], 0x6240u);
         uint8_t* const orow = outp;
         outp += p.out_pitch;
+        auto store_row = [&]() {
+          if constexpr (NW == 2) *reinterpret_cast<uint32_t*>(orow) = ow[0];
+          else *reinterpret_cast<uint2*>(orow) = make_uint2(ow[0], ow[NW / 2 - 1]);
+        };
         if constexpr (!MASKED) {
-          *reinterpret_cast<uint2*>(orow) = make_uint2(w0, w1);
+          store_row();
         } else if (yr < valid_h) {
-          if (x0 + rows::RCOLS <= valid_w) {
-            *reinterpret_cast<uint2*>(orow) = make_uint2(w0, w1);
+          if (x0 + NC <= valid_w) {
+            store_row();
           } else {
 #pragma unroll
-            for (int i = 0; i < rows::RCOLS; ++i)
-              if (x0 + i < valid_w) orow[i] = (uint8_t)((i < 4 ? w0 : w1) >> (8 * (i & 3)));
+            for (int i = 0; i < NC; ++i)
+              if (x0 + i < valid_w) orow[i] = (uint8_t)(ow[i >> 2] >> (8 * (i & 3)));
           }
         }
       };
       // output rows 2s, 2s + 1 of the thread: r0, r1 = sorted rows above / at 2s (carried), r2, r3 new
-      auto step = [&](int s, rows::Sorted& r0, rows::Sorted& r1, rows::Sorted& r2, rows::Sorted& r3) {
-        rows::sort_row(srow + (2 * s + 2) * G::BOXW, r2, one, m1);
-        uint32_t pm[4], qm[4];
+      auto step = [&](int s, Row& r0, Row& r1, Row& r2, Row& r3) {
+        sort_row<NW, MID_FMA>(srow + (2 * s + 2) * G::BOXW, r2, hi_byte, one, m1);
+        uint32_t pm[NW], qm[NW];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < NW; ++i) {
           pm[i] = vmin2(r1.mid[i], r2.mid[i]);
           qm[i] = vmax2(r1.mid[i], r2.mid[i]);
         }
         out_row(r0, r1, r2, pm, qm, r0.mid, y0 + 2 * s);
-        rows::sort_row(srow + (2 * s + 3) * G::BOXW, r3, one, m1);
+        sort_row<NW, MID_FMA>(srow + (2 * s + 3) * G::BOXW, r3, hi_byte, one, m1);
         out_row(r1, r2, r3, pm, qm, r3.mid, y0 + 2 * s + 1);
       };
       // two steps per iteration: the ring's roles swap without register moves
@@ -363,123 +373,8 @@ __global__ void __launch_bounds__(THREADS, FULL ? IRDN_K3_MINBLOCKS : 5) fnr_k3_
         step(s + 1, ring[2], ring[3], ring[0], ring[1]);
       }
     };
-    // FNR: column-first body (header of this file)
-    auto body_fnr = [&](auto masked) {
-      constexpr bool MASKED = decltype(masked)::value;
-      int valid_w = TW, valid_h = G::TH;
-      if constexpr (MASKED) {
-        valid_w = min(TW, p.width - ti.tx0);
-        valid_h = min(G::TH, p.row_end - ti.ty0);
-      }
-      uint8_t* outp = out_base + (int64_t)ti.b * p.out_frame + (int64_t)(ti.ty0 - p.row_begin + y0) * p.out_pitch +
-                      ti.tx0 + x0;
-      // smem row of tile row y is y + 1; the thread's segment starts at box column R + x0
-      const uint8_t* srow = s_in + y0 * G::BOXW + G::R + x0;
-      uint32_t A[COLS + 2];
-      {
-        RowSeg r0, r1;
-        load_seg(srow, r0);
-        load_seg(srow + G::BOXW, r1);
-        make_keys(r0, r1, A);
-      }
-  #pragma unroll (kStepUnroll)
-      for (int s = 0; s < BAND / 2; ++s) {
-        uint32_t B[COLS + 2];
-        {
-          RowSeg r1, r2;
-          load_seg(srow + (2 * s + 2) * G::BOXW, r1);
-          load_seg(srow + (2 * s + 3) * G::BOXW, r2);
-          make_keys(r1, r2, B);
-        }
-        uint32_t lo[COLS + 2], hi[COLS + 2], mid[COLS + 2], S[COLS + 2];
-  #pragma unroll
-        for (int c = 0; c < COLS + 2; ++c) {
-          if (IRDN_K3_S_FMA == 1 || (IRDN_K3_S_FMA == 2 && (c & 1)))
-            S[c] = shift_pair(A[c], B[c], k65536);  // rows y, y+1 (IMAD.HI + IMAD)
-          else
-            S[c] = tile::prmt(A[c], B[c], 0x5432u);  // rows y, y+1
-          lo[c] = vmin3(A[c], S[c], B[c]);
-          hi[c] = vmax3(A[c], S[c], B[c]);
-  #if IRDN_K3_MID_FMA
-          mid[c] = fma_sub(fma_sub(fma_add(B[c], one, fma_add(A[c], one, S[c])), m1, lo[c]), m1, hi[c]);
-  #else
-          mid[c] = A[c] + S[c] + B[c] - lo[c] - hi[c];
-  #endif
-          A[c] = B[c];
-        }
-        uint32_t rowmask = 0xFFFFFFFFu;  // partial tiles: lanes of rows inside the tile
-        if constexpr (MASKED) {
-          const int yr = y0 + 2 * s;
-          rowmask = (yr < valid_h ? 0x0000FFFFu : 0u) | (yr + 1 < valid_h ? 0xFFFF0000u : 0u);
-        }
-        uint32_t out[COLS];
-  #pragma unroll
-        for (int j = 0; j < COLS; j += 2) {
-          const uint32_t pm = vmin2(mid[j + 1], mid[j + 2]), qm = vmax2(mid[j + 1], mid[j + 2]);
-  #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int o = j + h;  // output column o: key columns o, o+1, o+2
-            const uint32_t md = vmax2(pm, vmin2(qm, mid[h == 0 ? j : j + 3]));
-            const uint32_t mxlo = vmax3(lo[o], lo[o + 1], lo[o + 2]);
-            const uint32_t mnhi = vmin3(hi[o], hi[o + 1], hi[o + 2]);
-            const uint32_t mn3 = vmin3(mxlo, md, mnhi), mx3 = vmax3(mxlo, md, mnhi);
-            uint32_t med;
-            if (IRDN_K3_FIN_FMA == 1 || (IRDN_K3_FIN_FMA == 2 && h == 1))
-              med = fma_sub(fma_sub(fma_add(mnhi, one, fma_add(mxlo, one, md)), m1, mn3), m1, mx3);
-            else
-              med = mxlo + md + mnhi - mn3 - mx3;
-            const uint32_t c = S[o + 1];
-            const uint32_t mn = vmin3(lo[o], lo[o + 1], lo[o + 2]), mx = vmax3(hi[o], hi[o + 1], hi[o + 2]);
-            uint32_t sflag = hfma_sat(hsub(mn, c), hsub(mx, c), F16_ONE);  // 1.0: noisy lane
-            const uint32_t dm = hsub(med, c);
-            out[o] = hfma(dm, sflag, c);
-            if constexpr (MASKED) {
-              const bool colok = x0 + o < valid_w;
-              sflag &= colok ? rowmask : 0u;
-            }
-            racc = hadd(racc, hmul_sat_abs(dm, sflag));
-            dacc = hadd(dacc, sflag);
-          }
-        }
-        // keys -> bytes: byte 0 of a key is the upper row's pixel, byte 2 the lower row's
-        uint32_t row_a[COLS / 4], row_b[COLS / 4];
-  #pragma unroll
-        for (int w = 0; w < COLS / 4; ++w) {
-          const uint32_t q01 = tile::prmt(out[4 * w], out[4 * w + 1], 0x6240u);
-          const uint32_t q23 = tile::prmt(out[4 * w + 2], out[4 * w + 3], 0x6240u);
-          row_a[w] = tile::prmt(q01, q23, 0x5410u);
-          row_b[w] = tile::prmt(q01, q23, 0x7632u);
-        }
-        if constexpr (!MASKED) {
-          *reinterpret_cast<uint4*>(outp) = make_uint4(row_a[0], row_a[1], row_a[2], row_a[3]);
-          *reinterpret_cast<uint4*>(outp + p.out_pitch) = make_uint4(row_b[0], row_b[1], row_b[2], row_b[3]);
-        } else {
-          const int yr = y0 + 2 * s;
-          const uint8_t* ba = reinterpret_cast<const uint8_t*>(row_a);
-          const uint8_t* bb = reinterpret_cast<const uint8_t*>(row_b);
-          if (x0 + COLS <= valid_w) {
-            if (yr < valid_h) *reinterpret_cast<uint4*>(outp) = make_uint4(row_a[0], row_a[1], row_a[2], row_a[3]);
-            if (yr + 1 < valid_h)
-              *reinterpret_cast<uint4*>(outp + p.out_pitch) = make_uint4(row_b[0], row_b[1], row_b[2], row_b[3]);
-          } else {
-  #pragma unroll
-            for (int i = 0; i < COLS; ++i) {
-              if (x0 + i < valid_w) {
-                if (yr < valid_h) outp[i] = ba[i];
-                if (yr + 1 < valid_h) outp[p.out_pitch + i] = bb[i];
-              }
-            }
-          }
-        }
-        outp += 2 * p.out_pitch;
-      }
-    };
-    auto run = [&](auto& body) {
-      if (FULL || (ti.tx0 + TW <= p.width && ti.ty0 + G::TH <= p.row_end)) body(std::false_type{});
-      else if constexpr (!FULL) body(std::true_type{});
-    };
-    if constexpr (FNR) run(body_fnr);
-    else run(body_mf);
+    if (FULL || (ti.tx0 + TW <= p.width && ti.ty0 + G::TH <= p.row_end)) body(std::false_type{});
+    else if constexpr (!FULL) body(std::true_type{});
     if constexpr (FNR) {
       det_total += hsum_lanes(dacc);
       rep_total += hsum_lanes(racc);
