@@ -155,6 +155,9 @@ NET_INSTR_PER_PAIR = {3: 30, 5: 172, 7: 514, 9: None, 11: 1833}
 # pair (tools/netgen/sepgen.py prints them), taken by MF always and by FNR tiles whose
 # flagged fraction exceeds DENSE_FRAC (fnr_fast.cuh dense_min_for)
 DENSE_INSTR_PER_PAIR = {5: 56.0, 7: 121.5}
+# of which emitted as a + b - min (one add, one IMAD: FMA pipe) instead of a second VIMNMX
+# (sepgen.py ADDSUB_FRAC = 0.3): the count above stays the method's min / max work
+DENSE_ADDSUB_PER_PAIR = {5: 6.5, 7: 15.0}
 DENSE_FRAC = {5: 0.20, 7: 0.18}
 # FNR tiles predicted dense take the detector from the sorted rows (fnr_dense.cuh FUSED):
 # window min / max shared within a group, the noisy test, the signal / changed lanes
@@ -182,6 +185,7 @@ def static_ops(cfg, detected_fraction: float, method: str = "fnr") -> dict:
                           f"({dense} instructions per two medians)"
                           + (" + extremum detector fused from the sorted rows" if method == "fnr" else ""),
                 "minmax_instr_per_px": round(per_pair / 2, 3), "minmax_lane_ops_per_px": round(per_pair, 3),
+                "maxima_as_add_sub_per_px": DENSE_ADDSUB_PER_PAIR[K] / 2,
                 "detected_fraction": round(detected_fraction, 4)}
     per_pair = (net or 0) if method == "mf" else det + (net or 0) * detected_fraction  # MF: every pixel, no detector
     return {"method": (f"generated selection network on every pixel pair ({net} instructions per two medians)"

@@ -40,7 +40,7 @@ constexpr int kDenseUnroll7 = IRDN_DENSE_UNROLL7, kDenseUnroll5 = IRDN_DENSE_UNR
 // Sorted window row of smem row `rowp` (pointing at the lane's first pixel): v[i] is the
 // i-th smallest of the k values around each pixel of the pair (u16x2 lanes).
 template <typename T, int K>
-__device__ __forceinline__ void sorted_row(const T* rowp, uint32_t (&v)[K], uint32_t k65536) {
+__device__ __forceinline__ void sorted_row(const T* rowp, uint32_t (&v)[K], uint32_t k65536, uint32_t m1) {
   constexpr int r = K / 2, J = (r + 1) / 2;
   uint32_t wd[2 * J + 1];
 #pragma unroll
@@ -48,8 +48,8 @@ __device__ __forceinline__ void sorted_row(const T* rowp, uint32_t (&v)[K], uint
 #pragma unroll
   for (int d = -r; d <= r; ++d)
     v[d + r] = (d & 1) == 0 ? wd[J + d / 2] : shift_pair(wd[J + (d - 1) / 2], wd[J + (d + 1) / 2], k65536);
-  if constexpr (K == 7) sep::sort7(v);
-  else sep::sort5(v);
+  if constexpr (K == 7) sep::sort7(v, m1);
+  else sep::sort5(v, m1);
 }
 
 // Store the medians `med` of output row y (tile coordinates): FNR stores only the flagged
@@ -101,7 +101,7 @@ __device__ __forceinline__ uint32_t dense_tile(const T* s_in, int c0, T* outp, i
   uint32_t replaced = 0;
   uint32_t sacc = 0, racc = 0;  // FUSED: per-lane counts of signal / replaced pixels (u16 lanes, <= rows)
   auto S = [&](int q, uint32_t (&v)[K]) {
-    if constexpr (K == 5 || K == 7) sorted_row<T, K>(base + q * BOXW, v, k65536);
+    if constexpr (K == 5 || K == 7) sorted_row<T, K>(base + q * BOXW, v, k65536, m1);
   };
   auto put = [&](int y, uint32_t med) {
     replaced += put_row<T>(outp + (int64_t)y * pitch, base + y * BOXW, med, y, valid_rows, ok0, ok1, flags, fnr);
@@ -125,10 +125,10 @@ __device__ __forceinline__ uint32_t dense_tile(const T* s_in, int c0, T* outp, i
       S(-3, Sm3);
       S(-2, t);
       S(-1, Sm1);
-      sep::merge7(t, Sm1, Pm2);
+      sep::merge7(t, Sm1, Pm2, m1);
       S(0, t);
       S(1, S1);
-      sep::merge7(t, S1, P0);
+      sep::merge7(t, S1, P0, m1);
       S(2, S2);
     }
 #pragma unroll (kDenseUnroll7)
@@ -138,24 +138,24 @@ __device__ __forceinline__ uint32_t dense_tile(const T* s_in, int c0, T* outp, i
       S(a + 4, S4);
       S(a + 5, S5);
       S(a + 6, S6);
-      sep::merge7(S2, S3, P2);
-      sep::merge7(S4, S5, P4);
+      sep::merge7(S2, S3, P2, m1);
+      sep::merge7(S4, S5, P4, m1);
       uint32_t c4[22], cA[8], cB[8];
-      sep::core4_7(P0, P2, c4);
-      sep::core6_7(c4, Pm2, cA);
-      sep::core6_7(c4, P4, cB);
+      sep::core4_7(P0, P2, c4, m1);
+      sep::core6_7(c4, Pm2, cA, m1);
+      sep::core6_7(c4, P4, cB, m1);
       if constexpr (FUSED) {
         // window rows: a-3 | a-2, a-1 | a .. a+3 (shared) | a+4 | a+5 | a+6
         const uint32_t tn = vmin2(P0[0], P2[0]), tx = vmax2(P0[13], P2[13]);
-        put_f(a, sep::final7(cA, Sm3), vmin3(tn, Sm3[0], Pm2[0]), vmax3(tx, Sm3[6], Pm2[13]));
-        put_f(a + 1, sep::final7(cA, S4), vmin3(tn, Pm2[0], S4[0]), vmax3(tx, Pm2[13], S4[6]));
-        put_f(a + 2, sep::final7(cB, Sm1), vmin3(tn, Sm1[0], P4[0]), vmax3(tx, Sm1[6], P4[13]));
-        put_f(a + 3, sep::final7(cB, S6), vmin3(tn, P4[0], S6[0]), vmax3(tx, P4[13], S6[6]));
+        put_f(a, sep::final7(cA, Sm3, m1), vmin3(tn, Sm3[0], Pm2[0]), vmax3(tx, Sm3[6], Pm2[13]));
+        put_f(a + 1, sep::final7(cA, S4, m1), vmin3(tn, Pm2[0], S4[0]), vmax3(tx, Pm2[13], S4[6]));
+        put_f(a + 2, sep::final7(cB, Sm1, m1), vmin3(tn, Sm1[0], P4[0]), vmax3(tx, Sm1[6], P4[13]));
+        put_f(a + 3, sep::final7(cB, S6, m1), vmin3(tn, P4[0], S6[0]), vmax3(tx, P4[13], S6[6]));
       } else {
-        put(a, sep::final7(cA, Sm3));
-        put(a + 1, sep::final7(cA, S4));
-        put(a + 2, sep::final7(cB, Sm1));
-        put(a + 3, sep::final7(cB, S6));
+        put(a, sep::final7(cA, Sm3, m1));
+        put(a + 1, sep::final7(cA, S4, m1));
+        put(a + 2, sep::final7(cB, Sm1, m1));
+        put(a + 3, sep::final7(cB, S6, m1));
       }
 #pragma unroll
       for (int i = 0; i < 14; ++i) {
@@ -178,7 +178,7 @@ __device__ __forceinline__ uint32_t dense_tile(const T* s_in, int c0, T* outp, i
       S(-2, Sm2);
       S(-1, t);
       S(0, S0);
-      sep::merge5(t, S0, Pm1);
+      sep::merge5(t, S0, Pm1, m1);
       S(1, S1);
     }
 #pragma unroll (kDenseUnroll5)
@@ -186,16 +186,16 @@ __device__ __forceinline__ uint32_t dense_tile(const T* s_in, int c0, T* outp, i
       uint32_t S2[5], S3[5], P1[10], c[6];
       S(a + 2, S2);
       S(a + 3, S3);
-      sep::merge5(S1, S2, P1);
-      sep::core4_5(Pm1, P1, c);
+      sep::merge5(S1, S2, P1, m1);
+      sep::core4_5(Pm1, P1, c, m1);
       if constexpr (FUSED) {
         // window rows: a-2 | a-1 .. a+2 (shared) | a+3
         const uint32_t tn = vmin2(Pm1[0], P1[0]), tx = vmax2(Pm1[9], P1[9]);
-        put_f(a, sep::final5(c, Sm2), vmin2(tn, Sm2[0]), vmax2(tx, Sm2[4]));
-        put_f(a + 1, sep::final5(c, S3), vmin2(tn, S3[0]), vmax2(tx, S3[4]));
+        put_f(a, sep::final5(c, Sm2, m1), vmin2(tn, Sm2[0]), vmax2(tx, Sm2[4]));
+        put_f(a + 1, sep::final5(c, S3, m1), vmin2(tn, S3[0]), vmax2(tx, S3[4]));
       } else {
-        put(a, sep::final5(c, Sm2));
-        put(a + 1, sep::final5(c, S3));
+        put(a, sep::final5(c, Sm2, m1));
+        put(a + 1, sep::final5(c, S3, m1));
       }
 #pragma unroll
       for (int i = 0; i < 10; ++i) Pm1[i] = P1[i];

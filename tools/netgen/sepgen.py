@@ -183,11 +183,50 @@ def schedule(d: Dag, outs: list[int]):
     return ops
 
 
+# Fraction of the full comparators (2-input min and max of the same operands, both live)
+# whose max is emitted as a + b - min (addsub() in select_nets.cuh: one add on either pipe and
+# one IMAD on the FMA pipe) instead of a second VIMNMX on the ALU pipe, which the dense stage
+# saturates (--addsub-frac=F).
+ADDSUB_FRAC = 0.3  # measured: c3 FNR 0.318 -> 0.299 ms (0.15: 0.310, 0.25: 0.303, 0.35: 0.308, 0.45: 0.307)
+
+
+def to_addsub(ops, frac):
+    """Turn an evenly spread `frac` of the eligible max ops into ("addsub", [a, b, min])."""
+    if frac <= 0:
+        return ops, 0
+    mins = {tuple(sorted(srcs)): dst for dst, kind, srcs in ops if kind == "min" and len(srcs) == 2}
+    elig = [i for i, (dst, kind, srcs) in enumerate(ops)
+            if kind == "max" and len(srcs) == 2 and tuple(sorted(srcs)) in mins]
+    want = int(round(frac * len(elig)))
+    if want <= 0:
+        return ops, 0
+    pick = {elig[(j * len(elig)) // want] for j in range(want)}
+    out, pending = [], {}
+    done = set()
+    for i, (dst, kind, srcs) in enumerate(ops):
+        if i in pick:
+            lo = mins[tuple(sorted(srcs))]
+            op = (dst, "addsub", [srcs[0], srcs[1], lo])
+            if lo in done:
+                out.append(op)
+            else:
+                pending[lo] = op  # emitted right after its min
+            done.add(dst)
+            continue
+        out.append((dst, kind, srcs))
+        done.add(dst)
+        if dst in pending:
+            out.append(pending.pop(dst))
+    assert not pending
+    return out, len(pick)
+
+
 def emit_block(name, inputs, builder, outspec):
     d = Dag()
     leaves = [[d.leaf(arr, i) for i in range(n)] for arr, n in inputs]
     outs = builder(d, leaves)
     ops = schedule(d, outs)
+    ops, nas = to_addsub(ops, ADDSUB_FRAC)
 
     def ref(i):
         n = d.nodes[i]
@@ -198,15 +237,20 @@ def emit_block(name, inputs, builder, outspec):
     if outspec == "inplace":
         arr, n = inputs[0]
         params = f"uint32_t (&{arr})[{n}]"
-        sig = f"__device__ __forceinline__ void {name}({params})"
+        sig = f"__device__ __forceinline__ void {name}({params}, uint32_t m1)"
     elif outspec == 1:
-        sig = f"__device__ __forceinline__ uint32_t {name}({params})"
+        sig = f"__device__ __forceinline__ uint32_t {name}({params}, uint32_t m1)"
     else:
-        sig = f"__device__ __forceinline__ void {name}({params}, uint32_t (&o)[{outspec}])"
-    lines.append(f"// {len(ops)} instructions")
+        sig = f"__device__ __forceinline__ void {name}({params}, uint32_t (&o)[{outspec}], uint32_t m1)"
+    lines.append(f"// {len(ops) - nas} min/max instructions" + (f" + {nas} maxima as a + b - min" if nas else ""))
     lines.append(sig + " {")
+    if not nas:
+        lines.append("  (void)m1;")
     fn = {("min", 2): "vmin2", ("max", 2): "vmax2", ("min", 3): "vmin3", ("max", 3): "vmax3"}
     for dst, kind, srcs in ops:
+        if kind == "addsub":
+            lines.append(f"  const uint32_t t{dst} = addsub({', '.join(ref(s) for s in srcs)}, m1);")
+            continue
         lines.append(f"  const uint32_t t{dst} = {fn[(kind, len(srcs))]}({', '.join(ref(s) for s in srcs)});")
     if outspec == "inplace":
         arr = inputs[0][0]
@@ -229,7 +273,7 @@ def simulate(d, ops, outs, env):
             val[i] = env[n[1]][n[2]]
     for dst, kind, srcs in ops:
         vs = [val[s] for s in srcs]
-        val[dst] = min(vs) if kind == "min" else max(vs)
+        val[dst] = vs[0] + vs[1] - vs[2] if kind == "addsub" else (min(vs) if kind == "min" else max(vs))
     return [val[o] for o in outs]
 
 
@@ -299,6 +343,10 @@ def check_groups():
 
 
 def main():
+    global ADDSUB_FRAC
+    for a in sys.argv[1:]:
+        if a.startswith("--addsub-frac="):
+            ADDSUB_FRAC = float(a.split("=", 1)[1])
     check_sort_nets()
     check_groups()
     out = [
@@ -313,18 +361,22 @@ def main():
         "namespace sep {",
         "",
     ]
-    totals = {}
+    totals, moved = {}, {}
     for k in (5, 7):
         for name, inputs, builder, outspec in blocks(k):
             code, d, outs, ops = emit_block(name, inputs, builder, outspec)
             check_block(name, inputs, d, outs, ops)
-            totals[name] = len(ops)
+            totals[name] = sum(1 for o in ops if o[1] != "addsub")
+            moved[name] = sum(1 for o in ops if o[1] == "addsub")
             out += [code, ""]
     out += ["}  // namespace sep", "}  // namespace irdn", ""]
     sys.stdout.write("\n".join(out))
     # instructions per output word (two pixels) of each group structure
     g7 = 4 * totals["sort7"] + 2 * totals["merge7"] + totals["core4_7"] + 2 * totals["core6_7"] + 4 * totals["final7"]
     g5 = 2 * totals["sort5"] + totals["merge5"] + totals["core4_5"] + 2 * totals["final5"]
+    m7 = 4 * moved["sort7"] + 2 * moved["merge7"] + moved["core4_7"] + 2 * moved["core6_7"] + 4 * moved["final7"]
+    m5 = 2 * moved["sort5"] + moved["merge5"] + moved["core4_5"] + 2 * moved["final5"]
+    sys.stderr.write(f"maxima as a + b - min per output word: k=7 {m7 / 4:.1f}, k=5 {m5 / 2:.1f}\n")
     sys.stderr.write(f"{totals}\nk=7: {g7 / 4:.1f} min/max instructions per output word (2 px) "
                      f"= {g7 / 8:.2f} per pixel\nk=5: {g5 / 2:.1f} per word = {g5 / 4:.2f} per pixel\n")
 
