@@ -360,7 +360,9 @@ __global__ void __launch_bounds__(THREADS, FULL ? IRDN_K3_MINBLOCKS : 5) fnr_k3_
 #pragma unroll
         for (int i = 0; i < NW; ++i) {
           pm[i] = vmin2(r1.mid[i], r2.mid[i]);
-          qm[i] = vmax2(r1.mid[i], r2.mid[i]);
+          // MF (ALU-pipe bound): the pair's max as a + b - min on the FMA pipe (c5 0.538 -> 0.531 ms)
+          if constexpr (FNR) qm[i] = vmax2(r1.mid[i], r2.mid[i]);
+          else qm[i] = fma_sub(fma_add(r1.mid[i], one, r2.mid[i]), m1, pm[i]);
         }
         out_row(r0, r1, r2, pm, qm, r0.mid, y0 + 2 * s);
         sort_row<NW, MID_FMA>(srow + (2 * s + 3) * G::BOXW, r3, hi_byte, one, m1);
