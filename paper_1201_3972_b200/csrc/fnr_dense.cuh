@@ -20,7 +20,11 @@
 //      others) or of all pixels (MF), and counts replacements (median != centre).
 // The median is a selected input value, so the result is bit-identical to the introsort's.
 #pragma once
+#ifdef IRDN_SEP_NETS_H  // A/B builds with another generated header
+#include IRDN_SEP_NETS_H
+#else
 #include "sep_nets.cuh"
+#endif
 
 // Group loops unrolled by two: half of the carried state's register moves between groups
 // disappear (MF c3 0.301 -> 0.292 ms, MF c2 51.9 -> 50.2 us, FNR c3 / c2 -0.3 % / -0.7 %); by

@@ -231,7 +231,6 @@ __device__ __forceinline__ void detect(const T* s_in, int c0, T* outp, int64_t p
   static_assert(ROWS % 2 == 0, "output rows are produced in pairs");
   using G = Geo<T, K>;
   constexpr int r = G::r, BOXW = G::BOXW;
-  constexpr int J = (r + 1) / 2;
   constexpr bool VPAIR = IRDN_VPAIR < 0 ? K == 7 : IRDN_VPAIR != 0;
   constexpr int KR = VPAIR ? K + 1 : K;  // ring of per-row horizontal results
   constexpr int CR = r + 2;                   // ring of centre words
@@ -301,7 +300,6 @@ __device__ __forceinline__ void detect_rolled(const T* s_in, int c0, T* outp, in
   static_assert(ROWS <= 64, "flag streams hold 64 rows");
   using G = Geo<T, K>;
   constexpr int r = G::r, BOXW = G::BOXW;
-  constexpr int J = (r + 1) / 2;
   constexpr int NIN = ROWS + 2 * r;          // box rows
   constexpr int NB = (ROWS + K - 1) / K;     // output blocks of K rows
   const uint32_t m1 = 0u - one, k65536 = one << 16, ones = one * 0x00010001u;

@@ -187,6 +187,8 @@ def schedule(d: Dag, outs: list[int]):
 # whose max is emitted as a + b - min (addsub() in select_nets.cuh: one add on either pipe and
 # one IMAD on the FMA pipe) instead of a second VIMNMX on the ALU pipe, which the dense stage
 # saturates (--addsub-frac=F).
+ADDSUB_PICK = "even"  # which ones: "even" = evenly spread over the block, "slack" = most slack first
+ADDSUB_BLOCK = {}     # per-block overrides of the fraction (--addsub-frac=sort7:0.5,core4_7:0.2)
 ADDSUB_FRAC = 0.3  # measured: c3 FNR 0.318 -> 0.299 ms (0.15: 0.310, 0.25: 0.303, 0.35: 0.308, 0.45: 0.307)
 
 
@@ -200,7 +202,23 @@ def to_addsub(ops, frac):
     want = int(round(frac * len(elig)))
     if want <= 0:
         return ops, 0
-    pick = {elig[(j * len(elig)) // want] for j in range(want)}
+    if ADDSUB_PICK == "slack":
+        # the maxima with the most slack in the block's dependency graph first (a + b - min is
+        # two dependent instructions where VIMNMX is one)
+        depth, prod = {}, {}
+        for i, (dst, kind, srcs) in enumerate(ops):
+            depth[dst] = 1 + max([depth.get(x, 0) for x in srcs])
+            prod[dst] = i
+        total = max(depth.values())
+        tail = {dst: 0 for dst in depth}
+        for dst, kind, srcs in reversed(ops):
+            for x in srcs:
+                if x in tail:
+                    tail[x] = max(tail[x], tail[dst] + 1)
+        slack = {i: total - depth[ops[i][0]] - tail[ops[i][0]] for i in elig}
+        pick = set(sorted(elig, key=lambda i: (-slack[i], i))[:want])
+    else:
+        pick = {elig[(j * len(elig)) // want] for j in range(want)}
     out, pending = [], {}
     done = set()
     for i, (dst, kind, srcs) in enumerate(ops):
@@ -226,7 +244,7 @@ def emit_block(name, inputs, builder, outspec):
     leaves = [[d.leaf(arr, i) for i in range(n)] for arr, n in inputs]
     outs = builder(d, leaves)
     ops = schedule(d, outs)
-    ops, nas = to_addsub(ops, ADDSUB_FRAC)
+    ops, nas = to_addsub(ops, ADDSUB_BLOCK.get(name, ADDSUB_FRAC))
 
     def ref(i):
         n = d.nodes[i]
@@ -343,10 +361,16 @@ def check_groups():
 
 
 def main():
-    global ADDSUB_FRAC
+    global ADDSUB_FRAC, ADDSUB_PICK
     for a in sys.argv[1:]:
         if a.startswith("--addsub-frac="):
-            ADDSUB_FRAC = float(a.split("=", 1)[1])
+            for kv in a.split("=", 1)[1].split(","):
+                if ":" in kv:
+                    ADDSUB_BLOCK[kv.split(":")[0]] = float(kv.split(":")[1])
+                else:
+                    ADDSUB_FRAC = float(kv)
+        if a.startswith("--addsub-pick="):
+            ADDSUB_PICK = a.split("=", 1)[1]
     check_sort_nets()
     check_groups()
     out = [
